@@ -1,0 +1,138 @@
+/*
+ * stmf_b200 — C ABI of the B200-native FastSTMF fitting engine (sm_100a).
+ *
+ * The reference (tropfact, a pure numpy package) has no native boundary; the
+ * boundary this library replaces is its plugin protocol below the public API:
+ *
+ *   run_fit(R, rank, strategy, config)        engine.py:313-348
+ *     strategy.orient(R, rng)                 strategies.py:324-337   (stays host/numpy)
+ *     random_acol_init(work, rank, q, rng)    engine.py:170-195       (RNG draws host/numpy,
+ *                                                                      residuation on device)
+ *     FitRun(work, U, V, config, wall_clock)  engine.py:240-310       -> stmf_create/stmf_set_factors
+ *     strategy.sweep(run, rng) x budget       strategies.py:339-344   -> stmf_run
+ *     orientation.restore(U, V)               engine.py:59-67         (host)
+ *
+ * The Python package paper_2205_06619_b200 binds it with ctypes (the binding a
+ * maintainer of tropfact would add is shown in INTEGRATION.md).  All matrices are
+ * in the work orientation, row-major, host pointers unless stated otherwise.
+ *
+ * Numerics: STMF_F64 reproduces the numpy oracle bit for bit
+ * (objective = np.sum(np.sort(|residuals|)), decisions f < err on those values);
+ * STMF_F32 computes every element in binary32 and defines the objective / column
+ * scores as the exact sum of the binary32 terms rounded once to binary64.
+ *
+ * Every function returns STMF_OK (0) or an error code; stmf_last_error() gives a
+ * thread-local message.  A session is not thread-safe; distinct sessions are.
+ */
+#ifndef STMF_B200_H
+#define STMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  STMF_OK = 0,
+  STMF_ERR_INVALID = 1,   /* bad argument: shape, rank, missing seed entry, ... (ValueError) */
+  STMF_ERR_CUDA = 2,      /* CUDA runtime failure (no device, launch error, ...)          */
+  STMF_ERR_OOM = 3,       /* device allocation failed                                      */
+  STMF_ERR_NUMERIC = 4,   /* exact-objective window violated / decision bound violated     */
+  STMF_ERR_CAPACITY = 5,  /* trajectory buffer too small                                   */
+  STMF_ERR_NCCL = 6       /* collective failure (sharded sessions)                         */
+};
+
+enum { STMF_F64 = 0, STMF_F32 = 1 };
+
+typedef struct stmf_session stmf_session;
+
+/* Last error message of the calling thread ("" if none). */
+const char* stmf_last_error(void);
+/* Library version string and the device architecture it was built for. */
+const char* stmf_version(void);
+
+/*
+ * Create a fitting session on `device` for the work matrix X (m x n, dtype
+ * STMF_F64 -> double, STMF_F32 -> float) with given-mask `mask` (m*n bytes,
+ * nonzero = given; values under the mask are ignored).  Uploads X once and builds
+ * the compacted row (CSR) and column (CSC) layouts on the device.
+ * Replaces FitRun.__init__'s ownership of R (engine.py:248-252) and enforces
+ * MaskedMatrix.validate_coverage (tropical.py:114-127): every row and column must
+ * hold a given entry (STMF_ERR_INVALID otherwise).
+ */
+int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank,
+                const void* X, const uint8_t* mask, int device);
+int stmf_destroy(stmf_session* s);
+
+/* Shape/size queries: out[0..4] = m, n, rank, given count, dtype. */
+int stmf_info(stmf_session* s, int64_t* out5);
+
+/*
+ * Install factors.  U is m x rank.  If V is NULL the device computes
+ * V = (-U)^T (x)* R (masked min-plus residuation), i.e. the second half of
+ * random_acol_init (engine.py:194 -> tropical.py:179-194); otherwise V (rank x n)
+ * is copied as is.
+ */
+int stmf_set_factors(stmf_session* s, const void* U, const void* V);
+int stmf_get_factors(stmf_session* s, void* U, void* V);
+
+/* approx_error(work, U, V) (tropical.py:214-222) of the installed factors. */
+int stmf_objective(stmf_session* s, double* err);
+
+/*
+ * run_fit's sweep loop (engine.py:328-344) with the ByRow / TD_A strategy
+ * (strategies.py:191-224, 339-344) on the installed factors, which are updated
+ * in place.  budget_sweeps < 0 = unset; budget_seconds <= 0 = unset (at least one
+ * must be set).  epsilon is relative to the post-init error (engine.py:330).
+ * The trajectory (engine.py:263, 286, 309-310) is written to traj_t/traj_err
+ * (capacity traj_cap).  counts[0..7] = {trajectory length, attempts, accepts,
+ * sweeps, row visits, evaluated candidate updates (incl. speculative),
+ * replica escalations, product passes}.
+ */
+int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, double epsilon,
+             double* traj_t, double* traj_err, int64_t traj_cap, int64_t* counts);
+
+/* ---- differential-test hooks (device results copied to host buffers) ---- */
+
+/* trop_matmul + argmax_grid at the given entries of the installed factors, in
+ * row-major given-entry order: P[g], arg[g], top2[g] (max over l != arg). */
+int stmf_product_given(stmf_session* s, void* P, int32_t* arg, void* top2);
+/* td_grid(work,U,V).sum(axis=0) (strategies.py:185): n doubles */
+int stmf_col_scores(stmf_session* s, double* scores);
+/* axis 0: v[j] = min_{i given} X[i,j] - vec[i]   (_residuate_row, engine.py:198-201)
+ * axis 1: u[i] = min_{j given} X[i,j] - vec[j]   (_residuate_col, engine.py:204-207) */
+int stmf_residuate(stmf_session* s, int axis, const void* vec, void* out);
+/*
+ * One F-ULF (op 0, engine.py:210-225) or F-URF (op 1, engine.py:228-237) update at
+ * (i, j, k) evaluated from the installed factors WITHOUT committing it: writes
+ * the updated column k of U (m values) and row k of V (n values) and the
+ * objective f.  STMF_ERR_INVALID if (i, j) is not given.
+ */
+int stmf_try_update(stmf_session* s, int op, int64_t i, int64_t j, int k, void* ucol,
+                    void* vrow, double* f);
+/* Same, committed when f < current error (FitRun._attempt, engine.py:278-295);
+ * *accepted receives 0/1. */
+int stmf_attempt(stmf_session* s, int op, int64_t i, int64_t j, int k, double* f,
+                 int* accepted);
+
+/*
+ * Sessionless dense max-plus product over ALL (i, j) (trop_matmul + argmax_grid,
+ * tropical.py:158-169, 260-262) — used by FactorPair.product() for prediction.
+ * U m x rank, V rank x n host arrays; P m x n (may be NULL), arg m x n int32 (may be NULL).
+ */
+int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, const void* V,
+                     void* P, int32_t* arg, int device);
+
+/*
+ * Microbench hook (config C5): masked max-plus product + error reduction over
+ * the given entries of the installed factors, `reps` times back to back on the
+ * session stream; *ms = average device time per rep (CUDA events), *err = the
+ * objective.  No fit state changes.
+ */
+int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, double* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STMF_B200_H */

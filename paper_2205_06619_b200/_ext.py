@@ -1,0 +1,261 @@
+"""ctypes binding of libstmf_b200.so (include/stmf_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA device
+is usable, every entry point raises.  ``build()`` compiles the library in-tree for
+sm_100a (nvcc cross-compiles without a GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO_DIR = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+INCLUDE = os.path.join(REPO_DIR, "include")
+SOURCES = ["stmf_api.cu"]
+HEADERS = ["stmf_kernels.cuh"]
+
+STMF_F64, STMF_F32 = 0, 1
+ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
+             5: "capacity", 6: "NCCL error"}
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+class StmfError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"stmf_b200 {ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (os.path.sep not in c or os.path.exists(c)):
+            return c
+    return "nvcc"
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into lib/libstmf_b200.so for sm_100a (in-tree)."""
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "stmf_b200.h")]
+    if not force and os.path.exists(LIB_PATH) and all(
+            os.path.getmtime(d) <= os.path.getmtime(LIB_PATH) for d in deps):
+        return LIB_PATH
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    tmp = LIB_PATH + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *srcs]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise StmfError(2, f"CUDA extension not built ({LIB_PATH} missing); run "
+                           "paper_2205_06619_b200._ext.build() — there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    L.stmf_last_error.restype = ctypes.c_char_p
+    L.stmf_version.restype = ctypes.c_char_p
+    sig = {
+        "stmf_create": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _int],
+        "stmf_destroy": [_vp],
+        "stmf_info": [_vp, _vp],
+        "stmf_set_factors": [_vp, _vp, _vp],
+        "stmf_get_factors": [_vp, _vp, _vp],
+        "stmf_objective": [_vp, ctypes.POINTER(_dbl)],
+        "stmf_run": [_vp, _i64, _dbl, _dbl, _vp, _vp, _i64, _vp],
+        "stmf_product_given": [_vp, _vp, _vp, _vp],
+        "stmf_col_scores": [_vp, _vp],
+        "stmf_residuate": [_vp, _int, _vp, _vp],
+        "stmf_try_update": [_vp, _int, _i64, _i64, _int, _vp, _vp, ctypes.POINTER(_dbl)],
+        "stmf_attempt": [_vp, _int, _i64, _i64, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_int)],
+        "stmf_bench_product": [_vp, _int, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)],
+        "stmf_trop_matmul": [_int, _i64, _int, _i64, _vp, _vp, _vp, _vp, _int],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = _int
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_destroy", "stmf_info",
+                    "stmf_set_factors", "stmf_get_factors", "stmf_objective", "stmf_run",
+                    "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
+                    "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul"]
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise StmfError(rc, lib().stmf_last_error().decode())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+def dtype_code(dtype) -> int:
+    dtype = np.dtype(dtype)
+    if dtype == np.float64:
+        return STMF_F64
+    if dtype == np.float32:
+        return STMF_F32
+    raise TypeError(f"unsupported dtype {dtype} (float64 or float32)")
+
+
+def trop_matmul(U, V, device: int | None = None, want_arg: bool = False):
+    """Dense max-plus product (and lowest argmax) of host arrays on the device."""
+    U = np.asarray(U)
+    dtype = np.float32 if U.dtype == np.float32 else np.float64
+    U = np.ascontiguousarray(U, dtype=dtype)
+    V = np.ascontiguousarray(V, dtype=dtype)
+    if U.ndim != 2 or V.ndim != 2 or U.shape[1] != V.shape[0]:
+        raise ValueError(f"inner dimensions differ: {U.shape} x {V.shape}")
+    m, r = U.shape
+    n = V.shape[1]
+    P = np.empty((m, n), dtype)
+    arg = np.empty((m, n), np.int32) if want_arg else None
+    _check(lib().stmf_trop_matmul(dtype_code(dtype), m, r, n, _p(U), _p(V), _p(P),
+                                  None if arg is None else _p(arg),
+                                  default_device() if device is None else int(device)))
+    return (P, arg) if want_arg else P
+
+
+def default_device() -> int:
+    for var in ("STMF_DEVICE", "LOCAL_RANK"):
+        if os.environ.get(var):
+            return int(os.environ[var])
+    return 0
+
+
+class Session:
+    """One device-resident fit state (work orientation).  Owns all device buffers."""
+
+    def __init__(self, X: np.ndarray, mask: np.ndarray, rank: int, device: int | None = None):
+        X = np.asarray(X)
+        self.dtype = np.dtype(X.dtype)
+        code = dtype_code(self.dtype)
+        Xc = np.ascontiguousarray(np.where(mask, X, 0), dtype=self.dtype)
+        Mc = np.ascontiguousarray(mask, dtype=np.uint8)
+        self.m, self.n = Xc.shape
+        self.rank = int(rank)
+        h = _vp()
+        _check(lib().stmf_create(ctypes.byref(h), code, self.m, self.n, self.rank, _p(Xc), _p(Mc),
+                                 default_device() if device is None else int(device)))
+        self._h = h
+        info = np.zeros(5, np.int64)
+        _check(lib().stmf_info(self._h, _p(info)))
+        self.given = int(info[3])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().stmf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # factors ---------------------------------------------------------------
+    def set_factors(self, U, V=None):
+        U = np.ascontiguousarray(U, dtype=self.dtype)
+        if U.shape != (self.m, self.rank):
+            raise ValueError(f"U shape {U.shape} != {(self.m, self.rank)}")
+        if V is not None:
+            V = np.ascontiguousarray(V, dtype=self.dtype)
+            if V.shape != (self.rank, self.n):
+                raise ValueError(f"V shape {V.shape} != {(self.rank, self.n)}")
+        _check(lib().stmf_set_factors(self._h, _p(U), None if V is None else _p(V)))
+
+    def get_factors(self):
+        U = np.empty((self.m, self.rank), self.dtype)
+        V = np.empty((self.rank, self.n), self.dtype)
+        _check(lib().stmf_get_factors(self._h, _p(U), _p(V)))
+        return U, V
+
+    def objective(self) -> float:
+        e = _dbl()
+        _check(lib().stmf_objective(self._h, ctypes.byref(e)))
+        return e.value
+
+    def run(self, budget_sweeps=None, budget_seconds=None, epsilon=1e-8, traj_cap=None):
+        if traj_cap is None:
+            sw = budget_sweeps if budget_sweeps is not None else 1000
+            traj_cap = 2 + (self.m + 1) * (sw + 1)
+        tt = np.empty(traj_cap, np.float64)
+        te = np.empty(traj_cap, np.float64)
+        counts = np.zeros(8, np.int64)
+        _check(lib().stmf_run(self._h, -1 if budget_sweeps is None else int(budget_sweeps),
+                              0.0 if budget_seconds is None else float(budget_seconds), float(epsilon),
+                              _p(tt), _p(te), traj_cap, _p(counts)))
+        L = int(counts[0])
+        keys = ("traj_len", "attempts", "accepts", "sweeps", "row_visits", "evaluated", "replicas",
+                "product_passes")
+        return tt[:L].copy(), te[:L].copy(), dict(zip(keys, (int(c) for c in counts)))
+
+    # diff-test hooks ------------------------------------------------------
+    def product_given(self):
+        P = np.empty(self.given, self.dtype)
+        top2 = np.empty(self.given, self.dtype)
+        arg = np.empty(self.given, np.int32)
+        _check(lib().stmf_product_given(self._h, _p(P), _p(arg), _p(top2)))
+        return P, arg, top2
+
+    def col_scores(self):
+        s = np.empty(self.n, np.float64)
+        _check(lib().stmf_col_scores(self._h, _p(s)))
+        return s
+
+    def residuate(self, axis: int, vec):
+        vec = np.ascontiguousarray(vec, dtype=self.dtype)
+        out = np.empty(self.n if axis == 0 else self.m, self.dtype)
+        _check(lib().stmf_residuate(self._h, axis, _p(vec), _p(out)))
+        return out
+
+    def try_update(self, op: int, i: int, j: int, k: int):
+        u = np.empty(self.m, self.dtype)
+        v = np.empty(self.n, self.dtype)
+        f = _dbl()
+        _check(lib().stmf_try_update(self._h, op, i, j, k, _p(u), _p(v), ctypes.byref(f)))
+        return u, v, f.value
+
+    def attempt(self, op: int, i: int, j: int, k: int):
+        f = _dbl()
+        acc = _int()
+        _check(lib().stmf_attempt(self._h, op, i, j, k, ctypes.byref(f), ctypes.byref(acc)))
+        return f.value, bool(acc.value)
+
+    def bench_product(self, reps: int = 10, flush_l2: bool = True):
+        ms = _dbl()
+        err = _dbl()
+        _check(lib().stmf_bench_product(self._h, reps, int(flush_l2), ctypes.byref(ms), ctypes.byref(err)))
+        return ms.value, err.value

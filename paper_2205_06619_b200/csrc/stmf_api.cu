@@ -1,0 +1,966 @@
+// stmf_api.cu — session management, the ByRow/TD_A sweep driver and the C ABI
+// (include/stmf_b200.h) of the B200-native FastSTMF fitting engine.
+//
+// Driver structure of one row visit (strategies.py:191-224), all on the session
+// stream; the host only reads back the per-batch decision data:
+//   1. product caches (U(x)V, argmax, second best) + column scores + TD_A column
+//      histograms, recomputed only after an acceptance (state unchanged otherwise);
+//      residuation statistics of the factor index that changed;
+//   2. candidate order: stable radix sort of the row's given columns by score;
+//   3. speculative batches of candidates from the SAME state (rejected attempts
+//      revert bit-exactly, engine.py:131-133): phase A (first residuation from
+//      top-2 statistics, O(m+n) per eval), phase B (second residuation + error,
+//      one pass over the given entries per group of evals); the first eval in
+//      reference order with f < err wins (FitRun._attempt, engine.py:283);
+//   4. commit: column k of U, row k of V.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "stmf_b200.h"
+#include "stmf_kernels.cuh"
+
+using namespace stmf;
+
+// ----------------------------------------------------------------------------
+// errors
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+struct StmfError {
+  int code;
+};
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      set_err(e_ == cudaErrorMemoryAllocation ? STMF_ERR_OOM : STMF_ERR_CUDA, "%s:%d %s: %s", \
+              __FILE__, __LINE__, #call, cudaGetErrorString(e_));                            \
+      throw StmfError{e_ == cudaErrorMemoryAllocation ? STMF_ERR_OOM : STMF_ERR_CUDA};       \
+    }                                                                                        \
+  } while (0)
+
+#define LAUNCH_CK() CK(cudaGetLastError())
+
+[[noreturn]] static void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  throw StmfError{code};
+}
+
+// ----------------------------------------------------------------------------
+// host helpers
+
+// value = (hi:lo) * 2^-F rounded to nearest even binary64
+static double fx_to_double(u64 hi, u64 lo, int F) {
+  if (hi == 0) return std::ldexp((double)lo, -F);  // u64 -> double is RN on x86-64
+  int top = 64 + 63 - __builtin_clzll(hi);
+  int sh = top - 52;  // >= 12
+  auto bit = [&](int p) -> u64 { return p >= 64 ? (hi >> (p - 64)) & 1u : (lo >> p) & 1u; };
+  u64 q;
+  if (sh >= 64) q = hi >> (sh - 64);
+  else q = (hi << (64 - sh)) | (lo >> sh);
+  q &= (1ull << 53) - 1;
+  q |= (1ull << 52);
+  int guard = (int)bit(sh - 1);
+  bool sticky = false;
+  for (int p = sh - 2; p >= 0 && !sticky; p--) sticky = bit(p) != 0;
+  if (guard && (sticky || (q & 1u))) q++;
+  return std::ldexp((double)q, sh - F);
+}
+
+// finest binary grid 2^-g of a binary32 value (lowest set bit of its exact value)
+static int f32_grid(float x) {
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  b &= 0x7fffffffu;
+  if (b == 0) return -1000;
+  uint32_t e = b >> 23, frac = b & 0x7fffffu;
+  uint32_t mant = e ? (frac | 0x800000u) : frac;
+  int ex = e ? (int)e - 150 : -149;  // value = mant * 2^ex
+  return -(ex + __builtin_ctz(mant));
+}
+
+static inline unsigned nblk(int64_t work, int per) { return (unsigned)((work + per - 1) / per); }
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// numpy pairwise-summation tree of a length-N array (structure depends on N only)
+struct PWTree {
+  std::vector<int64_t> loff;
+  std::vector<int32_t> llen, lnode, left, right, lvl_off, lvl_nodes;
+  int nnodes = 0, H = 0;
+  void build(int64_t N) {
+    loff.clear(); llen.clear(); lnode.clear(); left.clear(); right.clear();
+    lvl_off.clear(); lvl_nodes.clear();
+    std::vector<int> height;
+    std::vector<int64_t> noff, nlen;
+    // iterative DFS
+    struct Fr { int64_t off, n; int id; int stage; };
+    auto newnode = [&](int64_t off, int64_t n) {
+      noff.push_back(off); nlen.push_back(n); left.push_back(-1); right.push_back(-1); height.push_back(0);
+      return (int)noff.size() - 1;
+    };
+    std::vector<Fr> st;
+    int root = newnode(0, N);
+    st.push_back({0, N, root, 0});
+    while (!st.empty()) {
+      Fr& f = st.back();
+      if (f.n <= 128) {
+        loff.push_back(f.off); llen.push_back((int32_t)f.n); lnode.push_back(f.id);
+        st.pop_back();
+        continue;
+      }
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      if (f.stage == 0) {
+        f.stage = 1;
+        int l = newnode(f.off, n2);
+        left[f.id] = l;
+        Fr c{f.off, n2, l, 0};
+        st.push_back(c);
+      } else if (f.stage == 1) {
+        f.stage = 2;
+        int r = newnode(f.off + n2, f.n - n2);
+        right[f.id] = r;
+        Fr c{f.off + n2, f.n - n2, r, 0};
+        st.push_back(c);
+      } else {
+        height[f.id] = 1 + std::max(height[left[f.id]], height[right[f.id]]);
+        st.pop_back();
+      }
+    }
+    nnodes = (int)noff.size();
+    H = height[root];
+    lvl_off.assign(H + 1, 0);
+    std::vector<std::vector<int32_t>> lv(H + 1);
+    for (int i = 0; i < nnodes; i++)
+      if (height[i] > 0) lv[height[i]].push_back(i);
+    lvl_off[0] = 0;
+    for (int h = 1; h <= H; h++) {
+      lvl_off[h] = lvl_off[h - 1] + (int)lv[h].size();
+      for (int x : lv[h]) lvl_nodes.push_back(x);
+    }
+    // lvl_off[h-1]..lvl_off[h] are the nodes of height h; shift to 0-based list
+  }
+};
+
+// ----------------------------------------------------------------------------
+struct SessionBase {
+  virtual ~SessionBase() {}
+  int dtype = 0;
+  virtual void info(int64_t* out) = 0;
+  virtual void set_factors(const void* U, const void* V) = 0;
+  virtual void get_factors(void* U, void* V) = 0;
+  virtual double objective() = 0;
+  virtual void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te,
+                   int64_t cap, int64_t* counts) = 0;
+  virtual void product_given(void* P, int32_t* arg, void* top2) = 0;
+  virtual void col_scores(double* out) = 0;
+  virtual void residuate(int axis, const void* vec, void* out) = 0;
+  virtual void try_update(int op, int64_t i, int64_t j, int k, void* ucol, void* vrow, double* f,
+                          bool commit, int* accepted) = 0;
+  virtual void bench_product(int reps, int flush, double* ms, double* err) = 0;
+};
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t cnt) {
+    if (p) { cudaFree(p); p = nullptr; }
+    n = cnt;
+    if (cnt) CK(cudaMalloc(&p, cnt * sizeof(T)));
+  }
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+
+template <typename T>
+struct Session : SessionBase {
+  static constexpr bool kExact = sizeof(T) == 4;  // binary32: exact-sum semantics
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int64_t m = 0, n = 0, N = 0;
+  int rank = 0;
+  int nsm = 148;
+  // layout
+  DevBuf<int64_t> row_ptr, col_ptr;
+  DevBuf<int32_t> col_idx, row_idx;
+  DevBuf<T> xr, xc;
+  std::vector<int64_t> h_row_ptr, h_col_ptr;
+  int64_t max_rownnz = 0, max_colnnz = 0;
+  // factors
+  DevBuf<T> Ut, V;
+  bool have_factors = false;
+  // product caches
+  DevBuf<T> t1r, t2r, t1c, t2c;
+  DevBuf<uint8_t> agr, agc;
+  DevBuf<double> score;
+  DevBuf<int32_t> colhist;
+  // residuation statistics
+  DevBuf<T> cm1, cm2, rm1, rm2;
+  DevBuf<int32_t> cmarg, rmarg;
+  // candidates
+  DevBuf<u64> ckeys, ckeys2;
+  DevBuf<int32_t> cvals, cperm, cj, ck;
+  DevBuf<T> cx, xrow_dense;
+  // batch scratch
+  int Emax = 512;
+  DevBuf<T> vbuf, ubufB, ubufA, vbufB;
+  DevBuf<u64> acc;
+  DevBuf<int> chg, flags, findpos;
+  u64* h_acc = nullptr;
+  int* h_chg = nullptr;
+  int* h_flags = nullptr;
+  // replica
+  DevBuf<u64> res, res_sorted;
+  DevBuf<double> pwval;
+  DevBuf<int64_t> pw_loff;
+  DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
+  PWTree pw;
+  DevBuf<uint8_t> cubtmp;
+  size_t cubtmp_bytes = 0;
+  // numerics
+  int F = 60;
+  double exact_limit = INFINITY;
+  double beta_rel = 0;
+  // state
+  bool dirty = true;
+  std::vector<char> stats_dirty;
+  bool err_valid = false;
+  double err = 0;
+  int64_t n_product_passes = 0, n_escalations = 0;
+  std::vector<int> batch_sched;
+
+  ~Session() override {
+    if (h_acc) cudaFreeHost(h_acc);
+    if (h_chg) cudaFreeHost(h_chg);
+    if (h_flags) cudaFreeHost(h_flags);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void info(int64_t* out) override {
+    out[0] = m; out[1] = n; out[2] = rank; out[3] = N; out[4] = dtype;
+  }
+
+  void init(int64_t m_, int64_t n_, int rank_, const T* X, const uint8_t* mask, int device) {
+    m = m_; n = n_; rank = rank_;
+    dev = device;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    nsm = prop.multiProcessorCount;
+    if (const char* e = getenv("STMF_EMAX")) Emax = std::max(8, atoi(e));
+    batch_sched = {8, 32, 128, 512};
+    if (const char* e = getenv("STMF_BATCH")) {
+      batch_sched.clear();
+      const char* p = e;
+      while (*p) { batch_sched.push_back(std::max(1, atoi(p))); while (*p && *p != ',') p++; if (*p) p++; }
+    }
+    for (int& b : batch_sched) b = std::min(b, Emax);
+    // upload dense X + mask, build CSR/CSC, free the dense copies
+    DevBuf<T> dX;
+    DevBuf<uint8_t> dM;
+    dX.alloc((size_t)(m * n));
+    dM.alloc((size_t)(m * n));
+    CK(cudaMemcpyAsync(dX.p, X, sizeof(T) * m * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dM.p, mask, (size_t)(m * n), cudaMemcpyHostToDevice, st));
+    DevBuf<int64_t> rc, cc;
+    rc.alloc(m); cc.alloc(n);
+    row_ptr.alloc(m + 1); col_ptr.alloc(n + 1);
+    k_count_rows<<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dM.p, rc.p); LAUNCH_CK();
+    k_count_cols<<<nblk(n, 256), 256, 0, st>>>(m, n, dM.p, cc.p); LAUNCH_CK();
+    k_scan_ptr<<<1, 1024, 0, st>>>(m, rc.p, row_ptr.p); LAUNCH_CK();
+    k_scan_ptr<<<1, 1024, 0, st>>>(n, cc.p, col_ptr.p); LAUNCH_CK();
+    h_row_ptr.resize(m + 1); h_col_ptr.resize(n + 1);
+    CK(cudaMemcpyAsync(h_row_ptr.data(), row_ptr.p, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_col_ptr.data(), col_ptr.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    N = h_row_ptr[m];
+    if (N == 0) fail(STMF_ERR_INVALID, "empty matrix");
+    for (int64_t i = 0; i < m; i++) {
+      int64_t c = h_row_ptr[i + 1] - h_row_ptr[i];
+      if (c == 0) fail(STMF_ERR_INVALID, "row %lld has no given entries", (long long)i);
+      max_rownnz = std::max(max_rownnz, c);
+    }
+    for (int64_t j = 0; j < n; j++) {
+      int64_t c = h_col_ptr[j + 1] - h_col_ptr[j];
+      if (c == 0) fail(STMF_ERR_INVALID, "column %lld has no given entries", (long long)j);
+      max_colnnz = std::max(max_colnnz, c);
+    }
+    col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
+    k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
+    k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
+    // grid of the given data (binary32 mode)
+    if (kExact) {
+      int g = -1000;
+      for (int64_t a = 0; a < m * n; a++)
+        if (mask[a]) g = std::max(g, f32_grid((float)X[a]));
+      gridX = g;
+    }
+    // caches and scratch
+    Ut.alloc((size_t)rank * m); V.alloc((size_t)rank * n);
+    t1r.alloc(N); t2r.alloc(N); t1c.alloc(N); t2c.alloc(N); agr.alloc(N); agc.alloc(N);
+    score.alloc(n); colhist.alloc((size_t)n * rank);
+    cm1.alloc((size_t)rank * n); cm2.alloc((size_t)rank * n); cmarg.alloc((size_t)rank * n);
+    rm1.alloc((size_t)rank * m); rm2.alloc((size_t)rank * m); rmarg.alloc((size_t)rank * m);
+    ckeys.alloc(n); ckeys2.alloc(n); cvals.alloc(n); cperm.alloc(n);
+    cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
+    vbuf.alloc((size_t)Emax * n); ubufB.alloc((size_t)Emax * m);
+    ubufA.alloc((size_t)Emax * m); vbufB.alloc((size_t)Emax * n);
+    acc.alloc(4 * (size_t)Emax); chg.alloc(2 * (size_t)Emax); flags.alloc(4); findpos.alloc(2);
+    CK(cudaMallocHost(&h_acc, sizeof(u64) * 4 * Emax));
+    CK(cudaMallocHost(&h_chg, sizeof(int) * 2 * Emax));
+    CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
+    size_t b1 = 0, b2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)n, 0, 64, st));
+    if (!kExact) {
+      res.alloc(N); res_sorted.alloc(N);
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, b2, res.p, res_sorted.p, (int64_t)N, 0, 64, st));
+      pw.build(N);
+      pwval.alloc(pw.nnodes);
+      upload(pw_loff, pw.loff); upload(pw_llen, pw.llen); upload(pw_lnode, pw.lnode);
+      upload(pw_left, pw.left); upload(pw_right, pw.right);
+      upload(pw_lvloff, pw.lvl_off); upload(pw_lvlnodes, pw.lvl_nodes);
+      int depth = 26 + (int)std::ceil(std::log2((double)N + 1));
+      beta_rel = 1.01 * depth * std::ldexp(1.0, -53);
+    }
+    cubtmp_bytes = std::max(b1, b2);
+    cubtmp.alloc(cubtmp_bytes);
+    stats_dirty.assign(rank, 1);
+    CK(cudaStreamSynchronize(st));
+  }
+  int gridX = -1000;
+
+  template <typename E>
+  void upload(DevBuf<E>& d, const std::vector<E>& h) {
+    d.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), sizeof(E) * h.size(), cudaMemcpyHostToDevice, st));
+  }
+
+  unsigned warps_grid(int64_t lines) const {
+    int64_t blocks = (lines * 32 + 255) / 256;
+    int64_t cap = (int64_t)nsm * 16;
+    return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+  }
+
+  void set_factors(const void* Uh, const void* Vh) override {
+    const T* U = (const T*)Uh;
+    std::vector<T> ut((size_t)rank * m);
+    for (int64_t i = 0; i < m; i++)
+      for (int k = 0; k < rank; k++) ut[(size_t)k * m + i] = U[i * rank + k];
+    CK(cudaMemcpyAsync(Ut.p, ut.data(), sizeof(T) * ut.size(), cudaMemcpyHostToDevice, st));
+    if (kExact) {
+      int g = gridX;
+      for (auto v : ut) g = std::max(g, f32_grid((float)v));
+      if (Vh) {
+        const T* Vp = (const T*)Vh;
+        for (int64_t a = 0; a < (int64_t)rank * n; a++) g = std::max(g, f32_grid((float)Vp[a]));
+      }
+      g = std::max(g, 0);
+      if (g > 52) fail(STMF_ERR_NUMERIC, "binary32 data grid 2^-%d is too fine for the exact objective", g);
+      F = g;
+      exact_limit = std::ldexp(1.0, 53 - g);
+    } else {
+      F = 60;
+      exact_limit = INFINITY;
+    }
+    if (Vh) {
+      CK(cudaMemcpyAsync(V.p, Vh, sizeof(T) * (size_t)rank * n, cudaMemcpyHostToDevice, st));
+    } else {
+      // V = (-U)^T (x)* R  (random_acol_init, engine.py:194): rr of every column of U
+      for (int k = 0; k < rank; k++) {
+        k_line_min<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p + (size_t)k * m,
+                                                       V.p + (size_t)k * n);
+        LAUNCH_CK();
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    have_factors = true;
+    dirty = true;
+    stats_dirty.assign(rank, 1);
+    err_valid = false;
+  }
+
+  void get_factors(void* Uh, void* Vh) override {
+    need_factors();
+    std::vector<T> ut((size_t)rank * m);
+    CK(cudaMemcpyAsync(ut.data(), Ut.p, sizeof(T) * ut.size(), cudaMemcpyDeviceToHost, st));
+    if (Vh) CK(cudaMemcpyAsync(Vh, V.p, sizeof(T) * (size_t)rank * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (Uh) {
+      T* U = (T*)Uh;
+      for (int64_t i = 0; i < m; i++)
+        for (int k = 0; k < rank; k++) U[i * rank + k] = ut[(size_t)k * m + i];
+    }
+  }
+
+  void need_factors() {
+    if (!have_factors) fail(STMF_ERR_INVALID, "factors not set (call stmf_set_factors first)");
+  }
+
+  void check_flags() {
+    CK(cudaMemcpyAsync(h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_flags[0] & ~1 & 7) {
+      int f = h_flags[0];
+      fail(STMF_ERR_NUMERIC, "exact objective window violated (flags %d, grid 2^-%d)", f, F);
+    }
+    if (kExact && (h_flags[0] & 1)) fail(STMF_ERR_NUMERIC, "inexact fixed-point conversion in exact mode");
+  }
+
+  // product caches + scores + histograms + statistics of dirty factor indices
+  void ensure_caches() {
+    need_factors();
+    if (dirty) {
+      CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+      k_product_csr<T><<<warps_grid(m), 256, 0, st>>>(m, n, rank, row_ptr.p, col_idx.p, Ut.p, V.p, t1r.p, t2r.p,
+                                                        agr.p);
+      LAUNCH_CK();
+      if (kExact) {
+        CK(cudaMemsetAsync(colhist.p, 0, sizeof(int32_t) * (size_t)n * rank, st));
+        k_product_csc_exact<T><<<warps_grid(n), 256, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p,
+                                                                t1c.p, t2c.p, agc.p, score.p, colhist.p,
+                                                                exact_limit, flags.p);
+      } else {
+        k_product_csc_seq<T><<<nblk(n, 64), 64, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p, t1c.p,
+                                                          t2c.p, agc.p, score.p, colhist.p);
+        LAUNCH_CK();
+        if (n == 1) {
+          DevBuf<double> col;
+          col.alloc(m);
+          k_colscore_single<T><<<1, 32, 0, st>>>(m, col_ptr.p, row_idx.p, xc.p, t1c.p, col.p, score.p);
+          LAUNCH_CK();
+          CK(cudaStreamSynchronize(st));
+        }
+      }
+      LAUNCH_CK();
+      n_product_passes++;
+      if (kExact) check_flags();
+      dirty = false;
+    }
+    for (int k = 0; k < rank; k++) {
+      if (!stats_dirty[k]) continue;
+      k_line_stats<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p + (size_t)k * m,
+                                                        cm1.p + (size_t)k * n, cm2.p + (size_t)k * n,
+                                                        cmarg.p + (size_t)k * n);
+      LAUNCH_CK();
+      k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p + (size_t)k * n,
+                                                        rm1.p + (size_t)k * m, rm2.p + (size_t)k * m,
+                                                        rmarg.p + (size_t)k * m);
+      LAUNCH_CK();
+      stats_dirty[k] = 0;
+    }
+  }
+
+  // objective of the state "current factors with column k of U := a, row k of V := b"
+  double state_objective(int k, const T* a, const T* b) {
+    if (kExact) {
+      CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
+      CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+      k_objective<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k, a, b,
+                                                      acc.p, flags.p, F, exact_limit);
+      LAUNCH_CK();
+      CK(cudaMemcpyAsync(h_acc, acc.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
+      check_flags();
+      return fx_to_double(h_acc[1], h_acc[0], F);
+    }
+    return replica(k, a, b);
+  }
+
+  // numpy replica: np.sum(np.sort(|residuals|)) bit for bit (tropical.py:211)
+  double replica(int k, const T* a, const T* b) {
+    n_escalations++;
+    k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k, a, b,
+                                                    res.p);
+    LAUNCH_CK();
+    size_t bytes = cubtmp_bytes;
+    // residuals are >= 0: bits 63 is clear, sort on bits 0..62
+    CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res.p, res_sorted.p, (int64_t)N, 0, 63, st));
+    int nl = (int)pw.loff.size();
+    k_pw_leaves<<<nblk(nl, 128), 128, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, res_sorted.p, pwval.p);
+    LAUNCH_CK();
+    if (pw.H > 0) {
+      k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, pwval.p);
+      LAUNCH_CK();
+    }
+    double v;
+    CK(cudaMemcpyAsync(&v, pwval.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return v;
+  }
+
+  double objective() override {
+    ensure_caches();
+    if (!err_valid) {
+      err = state_objective(0, Ut.p, V.p);
+      err_valid = true;
+    }
+    return err;
+  }
+
+  // ---- candidates of row i ------------------------------------------------------
+  int64_t build_candidates(int64_t i) {
+    int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
+    k_cand_keys<<<nblk(nc, 256), 256, 0, st>>>(nc, col_idx.p + beg, score.p, ckeys.p, cvals.p);
+    LAUNCH_CK();
+    size_t bytes = cubtmp_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, bytes, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)nc, 0, 64, st));
+    unsigned nb = std::max(1u, std::min(nblk(nc, 256), 64u));
+    k_cand_build<T><<<nb, 256, sizeof(int32_t) * rank, st>>>(nc, rank, col_idx.p + beg, xr.p + beg, agr.p + beg,
+                                                             cperm.p, colhist.p, cj.p, ck.p, cx.p);
+    LAUNCH_CK();
+    dense_row(i);
+    return nc;
+  }
+
+  void dense_row(int64_t i) {
+    int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
+    k_fill<T><<<nblk(n, 256), 256, 0, st>>>(n, xrow_dense.p, (T)INFINITY);
+    LAUNCH_CK();
+    k_scatter_row<T><<<nblk(nc, 256), 256, 0, st>>>(nc, col_idx.p + beg, xr.p + beg, xrow_dense.p);
+    LAUNCH_CK();
+  }
+
+  // ---- one speculative batch: candidates cj/ck/cx[t0, t0+E) of row i ------------
+  void eval_batch(int64_t i, int64_t t0, int E) {
+    const int32_t* bj = cj.p + t0;
+    const int32_t* bk = ck.p + t0;
+    const T* bx = cx.p + t0;
+    u64* acc_ulf = acc.p;
+    u64* acc_urf = acc.p + 2 * (size_t)E;
+    int* chg_ulf = chg.p;
+    int* chg_urf = chg.p + E;
+    CK(cudaMemsetAsync(acc.p, 0, sizeof(u64) * 4 * E, st));
+    CK(cudaMemsetAsync(chg.p, 0, sizeof(int) * 2 * E, st));
+    CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+    k_phaseA_ulf<T><<<nblk((int64_t)E * n, 256), 256, 0, st>>>(n, E, i, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
+                                                                  xrow_dense.p, vbuf.p, chg_ulf);
+    LAUNCH_CK();
+    k_phaseA_urf_fill<T><<<nblk((int64_t)E * m, 256), 256, 0, st>>>(m, E, bj, bk, rm1.p, rm2.p, rmarg.p, ubufA.p);
+    LAUNCH_CK();
+    k_phaseA_urf_seed<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p);
+    LAUNCH_CK();
+    k_chk_vec<T><<<nblk((int64_t)E * m, 256), 256, 0, st>>>(m, E, bk, ubufA.p, Ut.p, chg_urf);
+    LAUNCH_CK();
+    constexpr int EG = 8;
+    int ng = (E + EG - 1) / EG;
+    k_phaseB<T, EG><<<warps_grid(m * ng), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, E, bk,
+                                                         vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf, flags.p, F,
+                                                         exact_limit);
+    LAUNCH_CK();
+    k_phaseB<T, EG><<<warps_grid(n * ng), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, E, bk,
+                                                         ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf, flags.p, F,
+                                                         exact_limit);
+    LAUNCH_CK();
+    CK(cudaMemcpyAsync(h_acc, acc.p, sizeof(u64) * 4 * E, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_chg, chg.p, sizeof(int) * 2 * E, cudaMemcpyDeviceToHost, st));
+    check_flags();
+  }
+
+  const T* eval_a(int op, int q) const { return op == 0 ? ubufB.p + (size_t)q * m : ubufA.p + (size_t)q * m; }
+  const T* eval_b(int op, int q) const { return op == 0 ? vbuf.p + (size_t)q * n : vbufB.p + (size_t)q * n; }
+
+  // decide eval (op, q) of the current batch against err; returns 1 = accept (f set)
+  int decide(int op, int q, int E, int k, double* f) {
+    if (!h_chg[op * E + q]) return 0;  // state reproduced bit for bit: f == err
+    u64 lo = h_acc[op * 2 * E + 2 * q], hi = h_acc[op * 2 * E + 2 * q + 1];
+    double A = fx_to_double(hi, lo, F);
+    if (kExact) {
+      *f = A;
+      return A < err;
+    }
+    // fp64: |A - S| <= dr*S + da; |numpy(S) - S| <= beta*S  ("decision bound")
+    int64_t L = op == 0 ? (max_rownnz + 31) / 32 : (max_colnnz + 31) / 32;
+    int64_t lines = op == 0 ? m : n;
+    double dr = (double)(L + 8) * std::ldexp(1.0, -53);
+    double da = (double)lines * std::ldexp(1.0, -F + 1);
+    double margin = 2.0 * ((dr + beta_rel) * std::max(A, err) + da);
+    if (A - margin >= err) return 0;
+    double fr = replica(k, eval_a(op, q), eval_b(op, q));
+    if (A + margin < err && !(fr < err))
+      fail(STMF_ERR_NUMERIC, "decision bound violated: A=%.17g replica=%.17g err=%.17g", A, fr, err);
+    *f = fr;
+    return fr < err;
+  }
+
+  void commit(int op, int q, int k) {
+    CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, eval_a(op, q), sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(V.p + (size_t)k * n, eval_b(op, q), sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
+    dirty = true;
+    stats_dirty[k] = 1;
+  }
+
+  // ---- run_fit sweep loop ----------------------------------------------------------
+  struct RunState {
+    bool wall;
+    double t0, budget_seconds;
+    int64_t cur_sweep;
+    double* tt; double* te; int64_t cap, len;
+    int64_t attempts, accepts, visits, evaluated;
+  };
+
+  double run_now(RunState& R) { return R.wall ? now_s() - R.t0 : (double)R.cur_sweep; }
+  bool out_of_time(RunState& R) { return R.wall && now_s() - R.t0 >= R.budget_seconds; }
+  void traj_append(RunState& R, double t, double e) {
+    if (R.len >= R.cap) fail(STMF_ERR_CAPACITY, "trajectory capacity %lld exceeded", (long long)R.cap);
+    R.tt[R.len] = t; R.te[R.len] = e; R.len++;
+  }
+
+  // byrow_sweep(run, i, "TD_A") (strategies.py:191-224)
+  void row_visit(RunState& R, int64_t i) {
+    ensure_caches();
+    int64_t nc = build_candidates(i);
+    R.visits++;
+    std::vector<int> hk;
+    int64_t t0 = 0;
+    size_t bi = 0;
+    while (t0 < nc) {
+      int E = (int)std::min<int64_t>(nc - t0, batch_sched[std::min(bi, batch_sched.size() - 1)]);
+      bi++;
+      eval_batch(i, t0, E);
+      hk.resize(E);
+      CK(cudaMemcpyAsync(hk.data(), ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      R.evaluated += 2 * (int64_t)E;
+      for (int q = 0; q < E; q++) {
+        for (int op = 0; op < 2; op++) {
+          R.attempts++;
+          double f;
+          if (decide(op, q, E, hk[q], &f)) {
+            commit(op, q, hk[q]);
+            err = f;
+            R.accepts++;
+            traj_append(R, run_now(R), err);
+            return;
+          }
+        }
+      }
+      if (out_of_time(R)) return;
+      t0 += E;
+    }
+  }
+
+  void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
+           int64_t* counts) override {
+    need_factors();
+    if (budget_sweeps < 0 && !(budget_seconds > 0)) fail(STMF_ERR_INVALID, "set budget_sweeps or budget_seconds");
+    RunState R{};
+    R.wall = budget_seconds > 0;
+    R.budget_seconds = budget_seconds;
+    R.t0 = now_s();
+    R.tt = tt; R.te = te; R.cap = cap;
+    int64_t pp0 = n_product_passes, esc0 = n_escalations;
+    objective();
+    traj_append(R, run_now(R), err);  // FitRun.__init__ (engine.py:263)
+    double eps = epsilon * err;       // engine.py:330
+    int64_t sweeps = 0;
+    if (err > 0.0) {
+      for (;;) {
+        if (budget_sweeps >= 0 && sweeps >= budget_sweeps) break;
+        if (out_of_time(R)) break;
+        R.cur_sweep = sweeps + 1;
+        double err_before = err;
+        for (int64_t i = 0; i < m; i++) {
+          if (out_of_time(R)) break;
+          row_visit(R, i);
+        }
+        sweeps++;
+        traj_append(R, run_now(R), err);  // mark_sweep_boundary (engine.py:309-310)
+        if (err_before - err < eps) break;
+      }
+    }
+    counts[0] = R.len; counts[1] = R.attempts; counts[2] = R.accepts; counts[3] = sweeps;
+    counts[4] = R.visits; counts[5] = R.evaluated; counts[6] = n_escalations - esc0;
+    counts[7] = n_product_passes - pp0;
+  }
+
+  // ---- diff-test hooks -----------------------------------------------------------
+  void product_given(void* P, int32_t* arg, void* top2) override {
+    ensure_caches();
+    std::vector<uint8_t> a(N);
+    if (P) CK(cudaMemcpyAsync(P, t1r.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
+    if (top2) CK(cudaMemcpyAsync(top2, t2r.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(a.data(), agr.p, N, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (arg)
+      for (int64_t p = 0; p < N; p++) arg[p] = a[p];
+  }
+
+  void col_scores(double* out) override {
+    ensure_caches();
+    CK(cudaMemcpyAsync(out, score.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void residuate(int axis, const void* vec, void* out) override {
+    int64_t lin = axis == 0 ? m : n, lout = axis == 0 ? n : m;
+    DevBuf<T> dv, dout;
+    dv.alloc(lin); dout.alloc(lout);
+    CK(cudaMemcpyAsync(dv.p, vec, sizeof(T) * lin, cudaMemcpyHostToDevice, st));
+    if (axis == 0)
+      k_line_min<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, dv.p, dout.p);
+    else
+      k_line_min<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, dv.p, dout.p);
+    LAUNCH_CK();
+    CK(cudaMemcpyAsync(out, dout.p, sizeof(T) * lout, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void try_update(int op, int64_t i, int64_t j, int k, void* ucol, void* vrow, double* f, bool commit_if_better,
+                  int* accepted) override {
+    if (i < 0 || i >= m || j < 0 || j >= n || k < 0 || k >= rank) fail(STMF_ERR_INVALID, "index out of range");
+    ensure_caches();
+    // locate (i, j) among the given entries of row i (host copy of nothing: search on device)
+    int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
+    std::vector<int32_t> cols(nc);
+    CK(cudaMemcpyAsync(cols.data(), col_idx.p + beg, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    auto it = std::lower_bound(cols.begin(), cols.end(), (int32_t)j);
+    if (it == cols.end() || *it != (int32_t)j) fail(STMF_ERR_INVALID, "entry (%lld, %lld) is missing", (long long)i, (long long)j);
+    int64_t p = beg + (it - cols.begin());
+    if (!err_valid) objective();
+    int32_t jj = (int32_t)j, kk = k;
+    CK(cudaMemcpyAsync(cj.p, &jj, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ck.p, &kk, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(cx.p, xr.p + p, sizeof(T), cudaMemcpyDeviceToDevice, st));
+    dense_row(i);
+    eval_batch(i, 0, 1);
+    CK(cudaStreamSynchronize(st));
+    double fv;
+    if (!h_chg[op]) {
+      fv = err;
+    } else if (kExact) {
+      fv = fx_to_double(h_acc[op * 2 + 1], h_acc[op * 2], F);
+    } else {
+      fv = replica(k, eval_a(op, 0), eval_b(op, 0));
+    }
+    if (ucol) CK(cudaMemcpyAsync(ucol, eval_a(op, 0), sizeof(T) * m, cudaMemcpyDeviceToHost, st));
+    if (vrow) CK(cudaMemcpyAsync(vrow, eval_b(op, 0), sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *f = fv;
+    if (commit_if_better) {
+      *accepted = fv < err;
+      if (*accepted) { commit(op, 0, k); err = fv; }
+    }
+  }
+
+  void bench_product(int reps, int flush, double* ms, double* errout) override {
+    ensure_caches();
+    DevBuf<uint8_t> scratch;
+    if (flush) scratch.alloc((size_t)256 << 20);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float total = 0;
+    for (int r = 0; r < reps; r++) {
+      if (flush) CK(cudaMemsetAsync(scratch.p, r & 0xff, scratch.n, st));
+      CK(cudaEventRecord(e0, st));
+      k_product_csr<T><<<warps_grid(m), 256, 0, st>>>(m, n, rank, row_ptr.p, col_idx.p, Ut.p, V.p, t1r.p, t2r.p,
+                                                        agr.p);
+      CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
+      k_objective<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, 0, Ut.p,
+                                                      V.p, acc.p, flags.p, F, exact_limit);
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float t;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      total += t;
+    }
+    LAUNCH_CK();
+    CK(cudaMemcpyAsync(h_acc, acc.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *ms = total / std::max(reps, 1);
+    *errout = fx_to_double(h_acc[1], h_acc[0], F);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+};
+
+struct stmf_session {
+  SessionBase* impl;
+};
+
+// ----------------------------------------------------------------------------
+// C ABI
+
+#define GUARD(body)                              \
+  try {                                          \
+    g_err.clear();                               \
+    body;                                        \
+    return STMF_OK;                              \
+  } catch (const StmfError& e) {                 \
+    return e.code;                               \
+  } catch (const std::bad_alloc&) {              \
+    return set_err(STMF_ERR_OOM, "host allocation failed"); \
+  }
+
+#define NEED(s) \
+  if (!(s) || !(s)->impl) return set_err(STMF_ERR_INVALID, "null session")
+
+template <typename T>
+static void trop_matmul_impl(int64_t m, int rank, int64_t n, const void* U, const void* V, void* P, int32_t* arg,
+                             int device) {
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevBuf<T> dU, dV, dP;
+  DevBuf<int32_t> dA;
+  dU.alloc((size_t)m * rank); dV.alloc((size_t)rank * n);
+  if (P) dP.alloc((size_t)m * n);
+  if (arg) dA.alloc((size_t)m * n);
+  CK(cudaMemcpyAsync(dU.p, U, sizeof(T) * m * rank, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dV.p, V, sizeof(T) * rank * n, cudaMemcpyHostToDevice, st));
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 7) / 8));
+  k_maxplus_dense<T><<<grid, dim3(32, 8), 0, st>>>(m, rank, n, dU.p, dV.p, dP.p, dA.p);
+  LAUNCH_CK();
+  if (P) CK(cudaMemcpyAsync(P, dP.p, sizeof(T) * m * n, cudaMemcpyDeviceToHost, st));
+  if (arg) CK(cudaMemcpyAsync(arg, dA.p, sizeof(int32_t) * m * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+}
+
+extern "C" {
+
+const char* stmf_last_error(void) { return g_err.c_str(); }
+
+const char* stmf_version(void) { return "stmf_b200 0.1.0 (sm_100a)"; }
+
+int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, const void* X,
+                const uint8_t* mask, int device) {
+  if (!out || !X || !mask) return set_err(STMF_ERR_INVALID, "null argument");
+  if (m <= 0 || n <= 0) return set_err(STMF_ERR_INVALID, "empty matrix");
+  if (rank < 1) return set_err(STMF_ERR_INVALID, "rank must be >= 1");
+  if (rank > 255) return set_err(STMF_ERR_INVALID, "rank must be <= 255");
+  if (m >= (1ll << 31) || n >= (1ll << 31)) return set_err(STMF_ERR_INVALID, "dimension too large");
+  if (dtype != STMF_F64 && dtype != STMF_F32) return set_err(STMF_ERR_INVALID, "unknown dtype %d", dtype);
+  *out = nullptr;
+  SessionBase* impl = nullptr;
+  try {
+    g_err.clear();
+    if (dtype == STMF_F64) {
+      auto* s = new Session<double>();
+      impl = s;
+      s->dtype = dtype;
+      s->init(m, n, rank, (const double*)X, mask, device);
+    } else {
+      auto* s = new Session<float>();
+      impl = s;
+      s->dtype = dtype;
+      s->init(m, n, rank, (const float*)X, mask, device);
+    }
+  } catch (const StmfError& e) {
+    delete impl;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    delete impl;
+    return set_err(STMF_ERR_OOM, "host allocation failed");
+  }
+  *out = new stmf_session{impl};
+  return STMF_OK;
+}
+
+int stmf_destroy(stmf_session* s) {
+  if (!s) return STMF_OK;
+  delete s->impl;
+  delete s;
+  return STMF_OK;
+}
+
+int stmf_info(stmf_session* s, int64_t* out5) {
+  NEED(s);
+  GUARD(s->impl->info(out5));
+}
+
+int stmf_set_factors(stmf_session* s, const void* U, const void* V) {
+  NEED(s);
+  if (!U) return set_err(STMF_ERR_INVALID, "U is required");
+  GUARD(s->impl->set_factors(U, V));
+}
+
+int stmf_get_factors(stmf_session* s, void* U, void* V) {
+  NEED(s);
+  GUARD(s->impl->get_factors(U, V));
+}
+
+int stmf_objective(stmf_session* s, double* err) {
+  NEED(s);
+  GUARD(*err = s->impl->objective());
+}
+
+int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, double epsilon, double* traj_t,
+             double* traj_err, int64_t traj_cap, int64_t* counts) {
+  NEED(s);
+  if (!traj_t || !traj_err || !counts) return set_err(STMF_ERR_INVALID, "null output buffer");
+  if (epsilon < 0) return set_err(STMF_ERR_INVALID, "epsilon must be >= 0");
+  GUARD(s->impl->run(budget_sweeps, budget_seconds, epsilon, traj_t, traj_err, traj_cap, counts));
+}
+
+int stmf_product_given(stmf_session* s, void* P, int32_t* arg, void* top2) {
+  NEED(s);
+  GUARD(s->impl->product_given(P, arg, top2));
+}
+
+int stmf_col_scores(stmf_session* s, double* scores) {
+  NEED(s);
+  GUARD(s->impl->col_scores(scores));
+}
+
+int stmf_residuate(stmf_session* s, int axis, const void* vec, void* out) {
+  NEED(s);
+  if (axis != 0 && axis != 1) return set_err(STMF_ERR_INVALID, "axis must be 0 or 1");
+  GUARD(s->impl->residuate(axis, vec, out));
+}
+
+int stmf_try_update(stmf_session* s, int op, int64_t i, int64_t j, int k, void* ucol, void* vrow, double* f) {
+  NEED(s);
+  if (op != 0 && op != 1) return set_err(STMF_ERR_INVALID, "op must be 0 (F-ULF) or 1 (F-URF)");
+  GUARD(s->impl->try_update(op, i, j, k, ucol, vrow, f, false, nullptr));
+}
+
+int stmf_attempt(stmf_session* s, int op, int64_t i, int64_t j, int k, double* f, int* accepted) {
+  NEED(s);
+  if (op != 0 && op != 1) return set_err(STMF_ERR_INVALID, "op must be 0 (F-ULF) or 1 (F-URF)");
+  GUARD(s->impl->try_update(op, i, j, k, nullptr, nullptr, f, true, accepted));
+}
+
+int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, const void* V, void* P,
+                     int32_t* arg, int device) {
+  if (!U || !V) return set_err(STMF_ERR_INVALID, "null argument");
+  if (m <= 0 || n <= 0 || rank < 1) return set_err(STMF_ERR_INVALID, "bad shape");
+  if (dtype == STMF_F64) { GUARD(trop_matmul_impl<double>(m, rank, n, U, V, P, arg, device)); }
+  if (dtype == STMF_F32) { GUARD(trop_matmul_impl<float>(m, rank, n, U, V, P, arg, device)); }
+  return set_err(STMF_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, double* err) {
+  NEED(s);
+  GUARD(s->impl->bench_product(reps, flush_l2, ms, err));
+}
+
+}  // extern "C"

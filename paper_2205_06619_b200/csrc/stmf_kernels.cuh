@@ -1,0 +1,658 @@
+// stmf_kernels.cuh — sm_100a device code of the FastSTMF fitting engine.
+//
+// Data layout in HBM (work orientation, m <= n after orient):
+//   CSR  row_ptr[m+1] (int64), col_idx[N] (int32), xr[N] (T)     given entries by row
+//   CSC  col_ptr[n+1] (int64), row_idx[N] (int32), xc[N] (T)     given entries by column
+//   Ut   rank x m  (column k of U contiguous: the F-ULF/F-URF update unit)
+//   V    rank x n
+//   per-state product caches, in both CSR and CSC order:
+//        t1[N] = (U(x)V)_ij, t2[N] = max_{l != arg} (U_il + V_lj), ag[N] = argmax (uint8)
+//   per-k residuation statistics (top-2 minima with argmin):
+//        colstats of (X_ij - U_ik) over i  -> cm1/cm2/cmarg (rank x n)
+//        rowstats of (X_ij - V_kj) over j  -> rm1/rm2/rmarg (rank x m)
+//
+// Every elementwise op is a single correctly rounded IEEE add/sub or an exact
+// max/min/abs, so products, argmax, residuations and residuals are bit-identical
+// to numpy (T = double) or to the binary32 restatement (T = float).
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace stmf {
+
+typedef unsigned long long u64;
+
+// ----------------------------------------------------------------------------
+// scalar helpers (explicit _rn intrinsics: no contraction, no fast-math)
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double vabs(double a) { return fabs(a); }
+__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+template <typename T> __device__ __forceinline__ T tinf();
+template <> __device__ __forceinline__ double tinf<double>() { return CUDART_INF; }
+template <> __device__ __forceinline__ float tinf<float>() { return CUDART_INF_F; }
+__device__ __forceinline__ double shfl_xor(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ float shfl_xor(float v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
+// ----------------------------------------------------------------------------
+// 128-bit fixed point (LSB 2^-F) used for every cross-thread error reduction.
+// fp32 mode: F = data grid g (all values are multiples of 2^-g), the
+// per-line fp64 partials are exact and the conversion below is exact.
+// fp64 mode: F = 60, conversion truncates (<= 2^-60 per line, in the bound).
+// flag bit 1: inexact conversion, bit 2: overflow / non-finite.
+__device__ __forceinline__ void fx_from_double(double x, int F, u64& hi, u64& lo, int& flag) {
+  u64 b = (u64)__double_as_longlong(x);
+  int e = (int)((b >> 52) & 0x7ff);
+  u64 mant = b & 0xFFFFFFFFFFFFFull;
+  hi = 0; lo = 0;
+  if (e == 0x7ff || (b >> 63)) { flag |= 2; return; }
+  if (e == 0) { if (mant == 0) return; e = 1; } else mant |= (1ull << 52);
+  int s = e - 1075 + F;
+  if (s >= 0) {
+    if (s > 74) { flag |= 2; return; }
+    if (s == 0) lo = mant;
+    else if (s < 64) { lo = mant << s; hi = mant >> (64 - s); }
+    else hi = mant << (s - 64);
+  } else {
+    int t = -s;
+    if (t >= 64) { if (mant) flag |= 1; return; }
+    lo = mant >> t;
+    if (mant & ((1ull << t) - 1)) flag |= 1;
+  }
+}
+
+__device__ __forceinline__ void fx_atomic_add(u64* acc, u64 hi, u64 lo) {
+  if (lo) {
+    u64 old = atomicAdd(acc, lo);
+    if (old + lo < old) hi += 1;
+  }
+  if (hi) atomicAdd(acc + 1, hi);
+}
+
+// ----------------------------------------------------------------------------
+// Build kernels: dense X + byte mask -> CSR / CSC (given entries, index order).
+
+__global__ void k_count_rows(int64_t m, int64_t n, const uint8_t* __restrict__ mask,
+                             int64_t* __restrict__ cnt) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    int64_t c = 0;
+    for (int64_t j = lane; j < n; j += 32) c += mask[r * n + j] != 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+
+__global__ void k_count_cols(int64_t m, int64_t n, const uint8_t* __restrict__ mask,
+                             int64_t* __restrict__ cnt) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t c = 0;
+  for (int64_t r = 0; r < m; r++) c += mask[r * n + j] != 0;
+  cnt[j] = c;
+}
+
+// exclusive scan of cnt[0..len) into ptr[0..len] (single block, len small: m or n)
+__global__ void k_scan_ptr(int64_t len, const int64_t* __restrict__ cnt, int64_t* __restrict__ ptr) {
+  __shared__ int64_t part[1024];
+  int t = threadIdx.x, nt = blockDim.x;
+  int64_t per = (len + nt - 1) / nt;
+  int64_t b = t * per, e = b + per < len ? b + per : len;
+  int64_t s = 0;
+  for (int64_t i = b; i < e; i++) s += cnt[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < nt; i++) { int64_t v = part[i]; part[i] = run; run += v; }
+    ptr[len] = run;
+  }
+  __syncthreads();
+  int64_t run = part[t];
+  for (int64_t i = b; i < e; i++) { ptr[i] = run; run += cnt[i]; }
+}
+
+template <typename T>
+__global__ void k_fill_csr(int64_t m, int64_t n, const T* __restrict__ X, const uint8_t* __restrict__ mask,
+                           const int64_t* __restrict__ ptr, int32_t* __restrict__ idx, T* __restrict__ xv) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    int64_t pos = ptr[r];
+    for (int64_t j0 = 0; j0 < n; j0 += 32) {
+      int64_t j = j0 + lane;
+      bool g = j < n && mask[r * n + j] != 0;
+      unsigned bal = __ballot_sync(0xffffffffu, g);
+      if (g) {
+        int64_t p = pos + __popc(bal & ((1u << lane) - 1));
+        idx[p] = (int32_t)j;
+        xv[p] = X[r * n + j];
+      }
+      pos += __popc(bal);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_fill_csc(int64_t m, int64_t n, const T* __restrict__ X, const uint8_t* __restrict__ mask,
+                           const int64_t* __restrict__ ptr, int32_t* __restrict__ idx, T* __restrict__ xv) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t p = ptr[j];
+  for (int64_t r = 0; r < m; r++)
+    if (mask[r * n + j]) { idx[p] = (int32_t)r; xv[p] = X[r * n + j]; p++; }
+}
+
+// ----------------------------------------------------------------------------
+// Product caches.  CSR pass: warp per row (U_r. is warp-uniform).
+
+template <typename T>
+__device__ __forceinline__ void top2_entry(const T* __restrict__ Ut, const T* __restrict__ V, int64_t m,
+                                           int64_t n, int rank, int64_t r, int64_t c, T& b1, T& b2, int& a) {
+  b1 = add_rn(Ut[r], V[c]);
+  b2 = -tinf<T>();
+  a = 0;
+  for (int l = 1; l < rank; l++) {
+    T s = add_rn(Ut[(int64_t)l * m + r], V[(int64_t)l * n + c]);
+    if (s > b1) { b2 = b1; b1 = s; a = l; }
+    else b2 = vmax(b2, s);
+  }
+}
+
+template <typename T>
+__global__ void k_product_csr(int64_t m, int64_t n, int rank, const int64_t* __restrict__ ptr,
+                              const int32_t* __restrict__ idx, const T* __restrict__ Ut, const T* __restrict__ V,
+                              T* __restrict__ t1, T* __restrict__ t2, uint8_t* __restrict__ ag) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+      T b1, b2; int a;
+      top2_entry(Ut, V, m, n, rank, r, (int64_t)idx[p], b1, b2, a);
+      t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a;
+    }
+  }
+}
+
+// CSC pass, fp64 oracle-compat: thread per column, rows ascending, so the column
+// score is summed exactly in numpy's td_grid(...).sum(axis=0) order
+// (strategies.py:185: sequential over rows).  Also the TD_A column histogram.
+template <typename T>
+__global__ void k_product_csc_seq(int64_t m, int64_t n, int rank, const int64_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ idx, const T* __restrict__ xc,
+                                  const T* __restrict__ Ut, const T* __restrict__ V, T* __restrict__ t1,
+                                  T* __restrict__ t2, uint8_t* __restrict__ ag, double* __restrict__ score,
+                                  int32_t* __restrict__ colhist) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double s = 0.0;
+  int32_t* h = colhist + c * rank;
+  for (int l = 0; l < rank; l++) h[l] = 0;
+  for (int64_t p = ptr[c]; p < ptr[c + 1]; p++) {
+    T b1, b2; int a;
+    top2_entry(Ut, V, m, n, rank, (int64_t)idx[p], c, b1, b2, a);
+    t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a;
+    s = __dadd_rn(s, (double)vabs(sub_rn(xc[p], b1)));
+    h[a] += 1;
+  }
+  score[c] = s;
+}
+
+// CSC pass, exact mode: warp per column; the fp64 partials of binary32 terms on
+// the 2^-g grid are exact below 2^(53-g) (checked: flag bit 4), so the warp sum
+// is the exact column score, order independent.
+template <typename T>
+__global__ void k_product_csc_exact(int64_t m, int64_t n, int rank, const int64_t* __restrict__ ptr,
+                                    const int32_t* __restrict__ idx, const T* __restrict__ xc,
+                                    const T* __restrict__ Ut, const T* __restrict__ V, T* __restrict__ t1,
+                                    T* __restrict__ t2, uint8_t* __restrict__ ag, double* __restrict__ score,
+                                    int32_t* __restrict__ colhist, double exact_limit, int* __restrict__ flags) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w; c < n; c += nw) {
+    double s = 0.0;
+    for (int64_t p = ptr[c] + lane; p < ptr[c + 1]; p += 32) {
+      T b1, b2; int a;
+      top2_entry(Ut, V, m, n, rank, (int64_t)idx[p], c, b1, b2, a);
+      t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a;
+      s = __dadd_rn(s, (double)vabs(sub_rn(xc[p], b1)));
+      atomicAdd(&colhist[c * rank + a], 1);
+    }
+    for (int o = 16; o; o >>= 1) s = __dadd_rn(s, shfl_xor(s, o));
+    if (lane == 0) {
+      if (!(s < exact_limit)) atomicOr(flags, 4);
+      score[c] = s;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Residuation statistics for factor index k (top-2 minima + argmin).
+template <typename T>
+struct Top2 { T m1, m2; int a1; };
+
+template <typename T>
+__device__ __forceinline__ void top2_push(Top2<T>& t, T d, int idx) {
+  if (d < t.m1) { t.m2 = t.m1; t.m1 = d; t.a1 = idx; }
+  else t.m2 = vmin(t.m2, d);
+}
+
+template <typename T>
+__device__ __forceinline__ Top2<T> top2_merge(const Top2<T>& A, const Top2<T>& B) {
+  bool aw = (A.m1 < B.m1) || (A.m1 == B.m1 && A.a1 < B.a1);
+  Top2<T> R;
+  R.m1 = aw ? A.m1 : B.m1;
+  R.a1 = aw ? A.a1 : B.a1;
+  R.m2 = aw ? vmin(A.m2, B.m1) : vmin(B.m2, A.m1);
+  return R;
+}
+
+template <typename T>
+__device__ __forceinline__ Top2<T> top2_warp(Top2<T> t) {
+  for (int o = 16; o; o >>= 1) {
+    Top2<T> u;
+    u.m1 = shfl_xor(t.m1, o);
+    u.m2 = shfl_xor(t.m2, o);
+    u.a1 = __shfl_xor_sync(0xffffffffu, t.a1, o);
+    t = top2_merge(t, u);
+  }
+  return t;
+}
+
+// lines = CSR rows (other = V row k)  or  CSC columns (other = Ut row k):
+// stats over entries p of line L of (x_p - other[idx_p]).
+template <typename T>
+__global__ void k_line_stats(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                             const T* __restrict__ xv, const T* __restrict__ other, T* __restrict__ s1,
+                             T* __restrict__ s2, int32_t* __restrict__ sarg) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t L = w; L < nlines; L += nw) {
+    Top2<T> t;
+    t.m1 = tinf<T>(); t.m2 = tinf<T>(); t.a1 = 0x7fffffff;
+    for (int64_t p = ptr[L] + lane; p < ptr[L + 1]; p += 32) {
+      int j = idx[p];
+      top2_push(t, sub_rn(xv[p], other[j]), j);
+    }
+    t = top2_warp(t);
+    if (lane == 0) { s1[L] = t.m1; s2[L] = t.m2; sarg[L] = t.a1; }
+  }
+}
+
+// plain residuation of an arbitrary vector: out[L] = min_p x_p - vec[idx_p]
+template <typename T>
+__global__ void k_line_min(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           const T* __restrict__ xv, const T* __restrict__ vec, T* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t L = w; L < nlines; L += nw) {
+    T mn = tinf<T>();
+    for (int64_t p = ptr[L] + lane; p < ptr[L + 1]; p += 32) mn = vmin(mn, sub_rn(xv[p], vec[idx[p]]));
+    for (int o = 16; o; o >>= 1) mn = vmin(mn, shfl_xor(mn, o));
+    if (lane == 0) out[L] = mn;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Candidate list of one row visit (_ranked_row_candidates + TD_A votes).
+
+__global__ void k_cand_keys(int64_t nc, const int32_t* __restrict__ cols, const double* __restrict__ score,
+                            u64* __restrict__ keys, int32_t* __restrict__ vals) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nc) return;
+  // scores are >= +0: their bit patterns are monotone; ~ gives descending order,
+  // the stable radix sort keeps ascending column order among equal scores
+  // (np.argsort(-scores[cols], kind="stable"), strategies.py:187).
+  keys[t] = ~(u64)__double_as_longlong(score[cols[t]]);
+  vals[t] = (int32_t)t;
+}
+
+template <typename T>
+__global__ void k_cand_build(int64_t nc, int rank, const int32_t* __restrict__ cols, const T* __restrict__ xrow,
+                             const uint8_t* __restrict__ agrow, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ colhist, int32_t* __restrict__ cj, int32_t* __restrict__ ck,
+                             T* __restrict__ cx) {
+  extern __shared__ int32_t rowhist[];
+  for (int l = threadIdx.x; l < rank; l += blockDim.x) rowhist[l] = 0;
+  __syncthreads();
+  for (int64_t p = threadIdx.x; p < nc; p += blockDim.x) atomicAdd(&rowhist[agrow[p]], 1);
+  __syncthreads();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc; t += (int64_t)gridDim.x * blockDim.x) {
+    int p = perm[t];
+    int j = cols[p];
+    const int32_t* h = colhist + (int64_t)j * rank;
+    int k = 0, best = -1;
+    for (int l = 0; l < rank; l++) {  // _vote: argmax of bincount, lowest index on ties
+      int v = rowhist[l] + h[l];
+      if (v > best) { best = v; k = l; }
+    }
+    cj[t] = j; ck[t] = k; cx[t] = xrow[p];
+  }
+}
+
+template <typename T>
+__global__ void k_fill(int64_t len, T* __restrict__ a, T v) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < len) a[t] = v;
+}
+
+template <typename T>
+__global__ void k_scatter_row(int64_t nc, const int32_t* __restrict__ cols, const T* __restrict__ x,
+                              T* __restrict__ dense) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < nc) dense[cols[t]] = x[t];
+}
+
+// ----------------------------------------------------------------------------
+// Phase A.  F-ULF evals q: v'_c = min(CM^(-i)_c, X_ic - s_q), s_q = X_ij - V_kj
+// (engine.py:222-223: U_ik <- X_ij - V_kj; V_k. <- rr(U_.k), with only u_i changed).
+template <typename T>
+__global__ void k_phaseA_ulf(int64_t n, int E, int64_t i, const int32_t* __restrict__ cj,
+                             const int32_t* __restrict__ ck, const T* __restrict__ cx, const T* __restrict__ V,
+                             const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
+                             const T* __restrict__ xrow_dense, T* __restrict__ vbuf, int* __restrict__ chg) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)E * n) return;
+  int q = (int)(t / n);
+  int64_t c = t - (int64_t)q * n;
+  int k = ck[q];
+  int64_t kn = (int64_t)k * n;
+  T s = sub_rn(cx[q], V[kn + cj[q]]);
+  T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
+  T v = vmin(cmx, sub_rn(xrow_dense[c], s));
+  vbuf[(int64_t)q * n + c] = v;
+  if (v != V[kn + c]) chg[q] = 1;
+}
+
+// F-URF evals q: u'_r = min(RM^(-j)_r, X_rj - s'_q), s'_q = X_ij - U_ik
+// (engine.py:234-235).  Fill from the row statistics, then the seed column.
+template <typename T>
+__global__ void k_phaseA_urf_fill(int64_t m, int E, const int32_t* __restrict__ cj, const int32_t* __restrict__ ck,
+                                  const T* __restrict__ rm1, const T* __restrict__ rm2,
+                                  const int32_t* __restrict__ rmarg, T* __restrict__ ubuf) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)E * m) return;
+  int q = (int)(t / m);
+  int64_t r = t - (int64_t)q * m;
+  int64_t km = (int64_t)ck[q] * m;
+  ubuf[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+}
+
+template <typename T>
+__global__ void k_phaseA_urf_seed(int64_t m, int E, int64_t i, const int32_t* __restrict__ cj,
+                                  const int32_t* __restrict__ ck, const T* __restrict__ cx,
+                                  const T* __restrict__ Ut, const int64_t* __restrict__ col_ptr,
+                                  const int32_t* __restrict__ row_idx, const T* __restrict__ xc,
+                                  T* __restrict__ ubuf) {
+  int q = blockIdx.x;
+  if (q >= E) return;
+  int j = cj[q];
+  int64_t km = (int64_t)ck[q] * m;
+  T s = sub_rn(cx[q], Ut[km + i]);
+  T* u = ubuf + (int64_t)q * m;
+  for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
+    int r = row_idx[p];
+    u[r] = vmin(u[r], sub_rn(xc[p], s));
+  }
+}
+
+template <typename T>
+__global__ void k_chk_vec(int64_t len, int E, const int32_t* __restrict__ ck, const T* __restrict__ buf,
+                          const T* __restrict__ cur, int* __restrict__ chg) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)E * len) return;
+  int q = (int)(t / len);
+  int64_t a = t - (int64_t)q * len;
+  if (buf[t] != cur[(int64_t)ck[q] * len + a]) chg[q] = 1;
+}
+
+// ----------------------------------------------------------------------------
+// Phase B — the hot kernel.  Work item = (line L, group of EG evals).  For each
+// eval q: line value w_q = min_p (x_p - vin_q[idx_p])  (the second residuation:
+// rc for F-ULF on CSR rows, rr for F-URF on CSC columns), then the eval's error
+// over the line: sum_p |x_p - max(Q^k_p, w_q + vin_q[idx_p])| with
+// Q^k_p = (ag_p == k) ? t2_p : t1_p  (U(x)V with column/row k replaced).
+// The line partial (fp64) goes to a 128-bit fixed-point accumulator per eval.
+template <typename T, int EG>
+__global__ void __launch_bounds__(256)
+k_phaseB(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+         const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
+         const uint8_t* __restrict__ ag, int E, const int32_t* __restrict__ ek, const T* __restrict__ vin,
+         int64_t len_other, const T* __restrict__ cur, T* __restrict__ out, u64* __restrict__ acc,
+         int* __restrict__ chg, int* __restrict__ flags, int F, double exact_limit) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int ngroups = (E + EG - 1) / EG;
+  int64_t items = nlines * ngroups;
+  for (int64_t it = w; it < items; it += nw) {
+    int g = (int)(it / nlines);  // group-major: concurrent warps share the same vin rows
+    int64_t L = it - (int64_t)g * nlines;
+    int e0 = g * EG;
+    int ne = E - e0 < EG ? E - e0 : EG;
+    const T* vq[EG];
+    int kq[EG];
+#pragma unroll
+    for (int q = 0; q < EG; q++) {
+      int e = e0 + (q < ne ? q : 0);
+      vq[q] = vin + (int64_t)e * len_other;
+      kq[q] = ek[e];
+    }
+    int64_t beg = ptr[L], end = ptr[L + 1];
+    T mn[EG];
+#pragma unroll
+    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
+    for (int64_t p = beg + lane; p < end; p += 32) {
+      T x = xv[p];
+      int c = idx[p];
+#pragma unroll
+      for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, __ldg(vq[q] + c)));
+    }
+#pragma unroll
+    for (int q = 0; q < EG; q++)
+      for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < EG; q++)
+        if (q < ne) {
+          out[(int64_t)(e0 + q) * nlines + L] = mn[q];
+          if (mn[q] != cur[(int64_t)kq[q] * nlines + L]) chg[e0 + q] = 1;
+        }
+    }
+    double part[EG];
+#pragma unroll
+    for (int q = 0; q < EG; q++) part[q] = 0.0;
+    for (int64_t p = beg + lane; p < end; p += 32) {
+      T x = xv[p];
+      int c = idx[p];
+      T a1 = t1[p], a2 = t2[p];
+      int a = ag[p];
+#pragma unroll
+      for (int q = 0; q < EG; q++) {
+        T Q = (a == kq[q]) ? a2 : a1;
+        T pm = vmax(Q, add_rn(mn[q], __ldg(vq[q] + c)));
+        part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EG; q++)
+      for (int o = 16; o; o >>= 1) part[q] = __dadd_rn(part[q], shfl_xor(part[q], o));
+    if (lane == 0) {
+      int fl = 0;
+#pragma unroll
+      for (int q = 0; q < EG; q++)
+        if (q < ne) {
+          if (!(part[q] < exact_limit)) fl |= 4;
+          u64 hi, lo;
+          fx_from_double(part[q], F, hi, lo, fl);
+          fx_atomic_add(acc + 2 * (e0 + q), hi, lo);
+        }
+      if (fl) atomicOr(flags, fl);
+    }
+  }
+}
+
+// Exact/bounded objective of an explicit state: entries' residual |x - max(Q^k, a_r + b_c)|
+// over CSR rows.  With a = Ut row k and b = V row k this is the current state.
+template <typename T>
+__global__ void k_objective(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                            const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
+                            const uint8_t* __restrict__ ag, int k, const T* __restrict__ a, const T* __restrict__ b,
+                            u64* __restrict__ acc, int* __restrict__ flags, int F, double exact_limit) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    double part = 0.0;
+    T ar = a[r];
+    for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+      T Q = (ag[p] == k) ? t2[p] : t1[p];
+      T pm = vmax(Q, add_rn(ar, b[idx[p]]));
+      part = __dadd_rn(part, (double)vabs(sub_rn(xv[p], pm)));
+    }
+    for (int o = 16; o; o >>= 1) part = __dadd_rn(part, shfl_xor(part, o));
+    if (lane == 0) {
+      int fl = 0;
+      if (!(part < exact_limit)) fl |= 4;
+      u64 hi, lo;
+      fx_from_double(part, F, hi, lo, fl);
+      fx_atomic_add(acc, hi, lo);
+      if (fl) atomicOr(flags, fl);
+    }
+  }
+}
+
+// numpy replica, step 1: the residual multiset of an explicit state (fp64 bit patterns).
+template <typename T>
+__global__ void k_residuals(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                            const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
+                            const uint8_t* __restrict__ ag, int k, const T* __restrict__ a, const T* __restrict__ b,
+                            u64* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    T ar = a[r];
+    for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+      T Q = (ag[p] == k) ? t2[p] : t1[p];
+      T pm = vmax(Q, add_rn(ar, b[idx[p]]));
+      out[p] = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
+    }
+  }
+}
+
+// numpy replica, step 3: pairwise-sum leaves (n <= 128) of the sorted residuals,
+// exactly numpy's DOUBLE_pairwise_sum leaf (8 strided accumulators + tail).
+__global__ void k_pw_leaves(int nleaves, const int64_t* __restrict__ loff, const int32_t* __restrict__ llen,
+                            const int32_t* __restrict__ lnode, const u64* __restrict__ sorted,
+                            double* __restrict__ val) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nleaves) return;
+  const double* a = reinterpret_cast<const double*>(sorted) + loff[t];
+  int n = llen[t];
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+  } else {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                    __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  }
+  val[lnode[t]] = res;
+}
+
+// numpy replica, step 4: combine internal nodes level by level (heights 1..H).
+__global__ void k_pw_combine(int H, const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ nodes,
+                             const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                             double* __restrict__ val) {
+  for (int h = 0; h < H; h++) {
+    for (int t = lvl_off[h] + threadIdx.x; t < lvl_off[h + 1]; t += blockDim.x) {
+      int nd = nodes[t];
+      val[nd] = __dadd_rn(val[left[nd]], val[right[nd]]);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace stmf
+
+namespace stmf {
+// Dense max-plus product over all entries (prediction path): block = 32 x 8 outputs
+// per pass; V tile of 32 columns x rank staged in shared memory, U row values are
+// warp-uniform broadcasts.
+template <typename T>
+__global__ void k_maxplus_dense(int64_t m, int rank, int64_t n, const T* __restrict__ U, const T* __restrict__ V,
+                                T* __restrict__ P, int32_t* __restrict__ arg) {
+  int64_t j = blockIdx.x * 32 + threadIdx.x;
+  int64_t i = blockIdx.y * 8 + threadIdx.y;
+  if (i >= m || j >= n) return;
+  const T* u = U + i * rank;
+  T best = add_rn(u[0], V[j]);
+  int a = 0;
+  for (int k = 1; k < rank; k++) {
+    T s = add_rn(u[k], V[(int64_t)k * n + j]);
+    if (s > best) { best = s; a = k; }
+  }
+  if (P) P[i * n + j] = best;
+  if (arg) arg[i * n + j] = a;
+}
+}  // namespace stmf
+
+namespace stmf {
+// numpy DOUBLE_pairwise_sum, single thread (recursive; depth ~ log2(n/128))
+__device__ double np_pairwise_dev(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_dev(a, n2), np_pairwise_dev(a + n2, n - n2));
+}
+
+// Column score of a single-column matrix (n == 1): numpy coalesces the unit axis
+// and reduces the whole td_grid column (zeros at missing rows) pairwise.
+template <typename T>
+__global__ void k_colscore_single(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                  const T* __restrict__ xc, const T* __restrict__ t1c, double* __restrict__ col,
+                                  double* __restrict__ score) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int64_t i = 0; i < m; i++) col[i] = 0.0;
+  for (int64_t p = ptr[0]; p < ptr[1]; p++) col[idx[p]] = (double)vabs(sub_rn(xc[p], t1c[p]));
+  score[0] = np_pairwise_dev(col, m);
+}
+}  // namespace stmf

@@ -1,0 +1,144 @@
+"""Fitting engine: host orientation/initialisation + the device-resident sweep loop.
+
+Mirrors the reference engine (engine.py) at its public names:
+  * ``random_acol_init`` — RNG draws and column means on the host with numpy (the
+    exact reference draw sequence, engine.py:170-195), the residuation
+    V = (-U)^T (x)* R on the device;
+  * ``run_fit`` — orient (host) -> init -> device sweeps -> restore (engine.py:313-348);
+  * ``f_ulf`` / ``f_urf`` — single updates computed on the device, mutating U, V in
+    place and returning an ``UpdateOutcome`` (engine.py:210-237).
+Only the FastSTMF strategy runs on the device path; everything else raises.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _ext
+from .types import (FactorPair, MaskedMatrix, Orientation, Permutation, RunConfig, Trajectory,
+                    UpdateOutcome)
+
+__all__ = ["FitSession", "random_acol_init", "acol_means", "run_fit", "f_ulf", "f_urf",
+           "stmf_baseline"]
+
+
+class FitSession(_ext.Session):
+    """Device state of one fit on a work-orientation ``MaskedMatrix``."""
+
+    def __init__(self, work: MaskedMatrix, rank: int, device: int | None = None):
+        super().__init__(work.values, work.mask, rank, device)
+
+
+def acol_means(R: MaskedMatrix, rank: int, columns: int, rng: np.random.Generator) -> np.ndarray:
+    """U of Random-Acol init: per factor column, the mean over given values of
+    ``q = min(columns, n)`` data columns drawn with replacement, falling back to the
+    row mean (engine.py:180-193).  Host numpy, same draws as the reference."""
+    if rank < 1:
+        raise ValueError("rank must be >= 1")
+    q = min(columns, R.n)
+    if q < 1:
+        raise ValueError("need at least one column to average")
+    row_fallback = R.row_means()
+    vals64 = R.values.astype(np.float64, copy=False)
+    U = np.empty((R.m, rank), dtype=np.float64)
+    for c in range(rank):
+        picks = rng.integers(0, R.n, size=q)
+        given = R.mask[:, picks]
+        vals = np.where(given, vals64[:, picks], 0.0)
+        counts = given.sum(axis=1)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            means = vals.sum(axis=1) / counts
+        U[:, c] = np.where(counts > 0, means, row_fallback)
+    return U.astype(R.dtype, copy=False)
+
+
+def random_acol_init(R: MaskedMatrix, rank: int, columns: int, rng: np.random.Generator,
+                     session: FitSession | None = None):
+    """(U, V) of Random-Acol initialisation; V residuated on the device."""
+    U = acol_means(R, rank, columns, rng)
+    own = session is None
+    s = FitSession(R, rank) if own else session
+    try:
+        s.set_factors(U)
+        _, V = s.get_factors()
+    finally:
+        if own:
+            s.close()
+    return U, V
+
+
+def _orient_faststmf(R: MaskedMatrix, rng: np.random.Generator):
+    """_SpecStrategy.orient for ByRow/RandPermR/wide (strategies.py:324-337)."""
+    transposed = R.m > R.n
+    work = R.transpose() if transposed else R.copy()
+    row_perm = Permutation.random(work.m, rng)
+    work = work.permute_rows(row_perm)
+    return work, Orientation(transposed, row_perm, None)
+
+
+def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int | None = None):
+    """Budgeted outer loop (engine.py:313-348) with the sweeps on the device.
+
+    ``strategy`` must be the FastSTMF strategy (``strategies.FASTSTMF`` or an object
+    with ``spec == FASTSTMF``); the device engine implements ByRow/TD_A only.
+    """
+    from .strategies import FASTSTMF
+    spec = getattr(strategy, "spec", strategy)
+    if spec != FASTSTMF:
+        raise NotImplementedError(
+            f"the B200 engine implements FastSTMF ({FASTSTMF.name}) only, not {getattr(spec, 'name', spec)!r}")
+    if rank != config.rank:
+        config = RunConfig(rank, config.budget_sweeps, config.budget_seconds, config.epsilon,
+                           config.acol_columns, config.seed, config.audit)
+    config.validate()
+    R.validate_coverage()
+    rng = np.random.default_rng(config.seed)
+    wall_clock = config.budget_seconds is not None
+    t0 = time.perf_counter()
+    work, orientation = _orient_faststmf(R, rng)
+    U0 = acol_means(work, rank, config.acol_columns, rng)
+    with FitSession(work, rank, device) as s:
+        s.set_factors(U0)
+        t_init = time.perf_counter() - t0 if wall_clock else 0.0
+        budget_seconds = None
+        if wall_clock:
+            budget_seconds = max(config.budget_seconds - (time.perf_counter() - t0), 1e-9)
+        tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)
+        U, V = s.get_factors()
+    t_max = config.budget_seconds if wall_clock else float(config.budget_sweeps)
+    traj = Trajectory(t_init=t_init, t_max=t_max, time_unit="seconds" if wall_clock else "sweeps")
+    for t, e in zip(tt.tolist(), te.tolist()):
+        traj.append(t + (t_init if wall_clock else 0.0), e)
+    traj.counts = counts
+    U_out, V_out = orientation.restore(U, V)
+    return FactorPair(U_out, V_out, rank, orientation), traj
+
+
+def _update(op: int, R: MaskedMatrix, U: np.ndarray, V: np.ndarray, i: int, j: int, k: int):
+    if not R.mask[i, j]:
+        raise ValueError(f"entry ({i}, {j}) is missing")
+    saved_col = U[:, k].copy()
+    saved_row = V[k, :].copy()
+    with FitSession(R, U.shape[1]) as s:
+        s.set_factors(U, V)
+        ucol, vrow, f = s.try_update(op, i, j, k)
+    U[:, k] = ucol
+    V[k, :] = vrow
+    return UpdateOutcome(f, k, saved_col, saved_row)
+
+
+def f_ulf(R: MaskedMatrix, U: np.ndarray, V: np.ndarray, i: int, j: int, k: int) -> UpdateOutcome:
+    """F-ULF at (i, j, k) on the device; mutates U, V (engine.py:210-225)."""
+    return _update(0, R, U, V, i, j, k)
+
+
+def f_urf(R: MaskedMatrix, U: np.ndarray, V: np.ndarray, i: int, j: int, k: int) -> UpdateOutcome:
+    """F-URF at (i, j, k) on the device; mutates U, V (engine.py:228-237)."""
+    return _update(1, R, U, V, i, j, k)
+
+
+def stmf_baseline(R: MaskedMatrix, rank: int, config: RunConfig):
+    """The original element-wise STMF (engine.py:351-385) is not on the B200 path."""
+    raise NotImplementedError("STMF baseline is not implemented by the B200 engine (FastSTMF only)")

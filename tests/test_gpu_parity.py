@@ -1,0 +1,142 @@
+"""Device parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden fixtures) and the CPU restatement (oracle/).  Bit-exact: products,
+argmax, residuations, objectives, factors and trajectories."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2205_06619_b200 as pkg
+from paper_2205_06619_b200 import _ext, engine
+from conftest import fit_case
+
+pytestmark = pytest.mark.gpu
+
+
+def session(X, M, U, V, rank=None):
+    s = _ext.Session(X, M, U.shape[1] if rank is None else rank)
+    s.set_factors(U, V)
+    return s
+
+
+def test_ops_match_reference(ops):
+    for c in range(int(ops["n_ops"])):
+        g = lambda k: ops[f"c{c}_{k}"]  # noqa: E731
+        X, M, U, V = g("X"), g("M"), g("U"), g("V")
+        if not M.any(axis=0).all() or not M.any(axis=1).all():
+            continue
+        with session(X, M, U, V) as s:
+            P, arg, _ = s.product_given()
+            assert np.array_equal(P, g("P")[M]), c
+            assert np.array_equal(arg, g("arg")[M]), c
+            assert np.array_equal(s.col_scores(), g("scores")), c
+            assert np.array_equal(s.residuate(0, g("u")), g("rr")), c
+            assert np.array_equal(s.residuate(1, g("v")), g("rc")), c
+            assert s.objective() == float(g("err")), c
+            i, j, k = (int(x) for x in g("ijk"))
+            for op, tag in ((0, "ulf"), (1, "urf")):
+                u, v, f = s.try_update(op, i, j, k)
+                assert np.array_equal(u, g(f"{tag}_U")[:, k]), (c, tag)
+                assert np.array_equal(v, g(f"{tag}_V")[k]), (c, tag)
+                assert f == float(g(f"{tag}_f")), (c, tag)
+
+
+def test_dense_product_and_argmax(ops):
+    for c in range(0, int(ops["n_ops"]), 3):
+        U, V = ops[f"c{c}_U"], ops[f"c{c}_V"]
+        P, arg = _ext.trop_matmul(U, V, want_arg=True)
+        assert np.array_equal(P, ops[f"c{c}_P"]) and np.array_equal(arg, ops[f"c{c}_arg"])
+
+
+def test_missing_seed_entry_raises(ops):
+    X, M, U, V = ops["c1_X"], ops["c1_M"].copy(), ops["c1_U"], ops["c1_V"]
+    gi, gj = np.nonzero(~M)
+    if gi.size == 0:
+        pytest.skip("fully given case")
+    with session(X, M, U, V) as s, pytest.raises(_ext.StmfError, match="missing"):
+        s.try_update(0, int(gi[0]), int(gj[0]), 0)
+
+
+@pytest.mark.parametrize("name", ["s0", "s1", "s2", "s3", "s4", "s5", "conv", "c1"])
+def test_fast_stmf_matches_reference(fits, name):
+    c = fit_case(fits, name)
+    R = pkg.MaskedMatrix(c["R"], c["M"])
+    cfg = pkg.RunConfig(rank=int(c["rank"]), budget_sweeps=int(c["sweeps"]), epsilon=float(c["epsilon"]),
+                        seed=int(c["seed"]))
+    pair, traj = pkg.fast_stmf(R, int(c["rank"]), cfg)
+    assert np.array_equal(np.array(traj.errors), c["traj_e"])
+    assert np.array_equal(np.array(traj.times), c["traj_t"])
+    assert np.array_equal(pair.U, c["U"]) and np.array_equal(pair.V, c["V"])
+
+
+def _f32_case(seed, m, n, r, frac):
+    rng = np.random.default_rng(seed)
+    A = rng.random((m, r)); B = rng.random((r, n))
+    X = (np.max(A[:, :, None] + B[None], axis=1) + rng.normal(0, 0.05, (m, n))).astype(np.float32)
+    M = rng.random((m, n)) >= frac
+    M[np.arange(m), rng.integers(0, n, m)] = True
+    M[rng.integers(0, m, n), np.arange(n)] = True
+    R = pkg.MaskedMatrix(X, M, dtype=np.float32)
+    work, _ = engine._orient_faststmf(R, np.random.default_rng(seed + 1))
+    U0 = engine.acol_means(work, r, 5, np.random.default_rng(seed + 2))
+    return work, U0
+
+
+@pytest.mark.parametrize("seed,m,n,r,frac,sweeps", [(1, 30, 50, 3, 0.3, 4), (2, 64, 200, 5, 0.7, 2),
+                                                     (3, 120, 90, 10, 0.5, 1)])
+def test_f32_fit_matches_restatement(seed, m, n, r, frac, sweeps):
+    work, U0 = _f32_case(seed, m, n, r, frac)
+    with _ext.Session(work.values, work.mask, r) as s:
+        s.set_factors(U0)
+        U0d, V0d = s.get_factors()
+        V0 = np.stack([oracle.residuate_row(work.values, work.mask, U0[:, k]) for k in range(r)])
+        assert np.array_equal(V0d, V0)
+        tt, te, counts = s.run(budget_sweeps=sweeps, epsilon=0.0)
+        U, V = s.get_factors()
+    ref = oracle.fit(work.values, work.mask, U0, V0, budget_sweeps=sweeps, epsilon=0.0)
+    assert np.array_equal(te, ref["traj_err"])
+    assert np.array_equal(U, ref["U"]) and np.array_equal(V, ref["V"])
+    assert counts["attempts"] == ref["attempts"] and counts["accepts"] == ref["accepts"]
+    P, _, _ = oracle.trop_matmul(U, V)
+    M = work.mask
+    assert te[-1] == math.fsum(np.abs(work.values[M] - P[M]).astype(np.float64).tolist())
+
+
+def test_f64_fit_matches_restatement_lognormal():
+    """A reduced config-2 shape (log2(1+lognormal), 50% hidden) vs the oracle."""
+    rng = np.random.default_rng(5)
+    X = np.log2(1 + rng.lognormal(0, 1, (60, 140)))
+    from paper_2205_06619_b200 import gen
+    R = gen.apply_mask(X, 0.5, seed=6)[0]
+    work, _ = engine._orient_faststmf(R, np.random.default_rng(9))
+    U0 = engine.acol_means(work, 5, 5, np.random.default_rng(10))
+    V0 = np.stack([oracle.residuate_row(work.values, work.mask, U0[:, k]) for k in range(5)])
+    with _ext.Session(work.values, work.mask, 5) as s:
+        s.set_factors(U0)
+        tt, te, counts = s.run(budget_sweeps=3, epsilon=0.0)
+        U, V = s.get_factors()
+    ref = oracle.fit(work.values, work.mask, U0, V0, budget_sweeps=3, epsilon=0.0)
+    assert np.array_equal(te, ref["traj_err"])
+    assert np.array_equal(U, ref["U"]) and np.array_equal(V, ref["V"])
+    assert counts["attempts"] == ref["attempts"]
+
+
+def test_attempt_commit_semantics(fits):
+    c = fit_case(fits, "s2")
+    X, M = c["work_X"], c["work_M"]
+    with session(X, M, c["U0"], c["V0"]) as s:
+        e0 = s.objective()
+        gi, gj = np.nonzero(M)
+        accepted = 0
+        for t in range(0, gi.size, max(1, gi.size // 40)):
+            f, acc = s.attempt(t % 2, int(gi[t]), int(gj[t]), t % int(c["rank"]))
+            e1 = s.objective()
+            assert (e1 == f < e0) if acc else (e1 == e0)
+            accepted += acc
+            e0 = e1
+        assert accepted > 0
+        U, V = s.get_factors()
+    with session(X, M, U, V) as s2:
+        assert s2.objective() == e0  # committed error == fresh objective of the state
