@@ -132,6 +132,18 @@ int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, c
  */
 int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, double* err);
 
+/* ---- measurement plumbing ---- */
+
+/* The session's cudaStream_t (all device work of the session is ordered on it). */
+int stmf_stream(stmf_session* s, void** stream);
+/* on != 0: bracket every launch of the candidate-evaluation kernel (phase B)
+ * with CUDA events and accumulate its device time (read via stmf_counters). */
+int stmf_set_profiling(stmf_session* s, int on);
+/* out8 = {kernel launches of this library (process-wide), CUB radix-sort calls
+ * (process-wide), phase-B launches, phase-B device ns (profiled), phase-B
+ * launches timed, product passes, replica evaluations, given entries}. */
+int stmf_counters(stmf_session* s, int64_t* out8);
+
 #ifdef __cplusplus
 }
 #endif

@@ -185,7 +185,7 @@ def fit(X, mask, U0, V0, budget_sweeps=None, budget_seconds=None, epsilon=1e-8,
         traj_cap = 2 + (m + 1) * (sweeps + 1)
     tt = np.empty(traj_cap, np.float64)
     te = np.empty(traj_cap, np.float64)
-    cnt = np.zeros(5, np.int64)
+    cnt = np.zeros(6, np.int64)
     rc = getattr(lib(), f"orc_fit_{_sfx(X.dtype)}")(
         m, U.shape[1], n, _p(X), _p(mask), _p(U), _p(V),
         -1 if budget_sweeps is None else int(budget_sweeps),
@@ -197,5 +197,5 @@ def fit(X, mask, U0, V0, budget_sweeps=None, budget_seconds=None, epsilon=1e-8,
     return {
         "U": U, "V": V, "traj_t": tt[:L].copy(), "traj_err": te[:L].copy(),
         "attempts": int(cnt[1]), "accepts": int(cnt[2]), "sweeps": int(cnt[3]),
-        "capped": bool(cnt[4]),
+        "capped": bool(cnt[4]), "row_visits": int(cnt[5]),
     }

@@ -170,7 +170,7 @@ typedef struct {
   const T* X; const uint8_t* mask; T* U; T* V;
   double err, t0, budget_seconds;
   int wall, capped, dirty;
-  int64_t cur_sweep, attempts, accepts, max_attempts;
+  int64_t cur_sweep, attempts, accepts, max_attempts, visits;
   double* traj_t; double* traj_err; int64_t traj_cap, traj_len; int overflow;
   /* scratch */
   T* buf; T* ucol; T* saved_col; T* saved_row;
@@ -287,6 +287,7 @@ int FN(orc_fit)(int64_t m, int r, int64_t n, const T* X, const uint8_t* mask, T*
       for (int64_t i = 0; i < m; i++) { /* _SpecStrategy.sweep (strategies.py:340-344) */
         if (FN(out_of_time)(&c)) break;
         FN(byrow)(&c, i);
+        if (!c.capped) c.visits++; /* completed row visits */
       }
       sweeps++;
       FN(traj_append)(&c, FN(now)(&c), c.err); /* mark_sweep_boundary (engine.py:309-310) */
@@ -298,6 +299,7 @@ int FN(orc_fit)(int64_t m, int r, int64_t n, const T* X, const uint8_t* mask, T*
   out_counts[2] = c.accepts;
   out_counts[3] = sweeps;
   out_counts[4] = c.capped;
+  out_counts[5] = c.visits;
   free(c.buf); free(c.ucol); free(c.saved_col); free(c.saved_row); free(c.arg);
   free(c.scores); free(c.colhist); free(c.rowhist); free(c.cands);
   return c.overflow ? -1 : 0;

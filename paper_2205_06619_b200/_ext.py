@@ -91,6 +91,9 @@ def lib():
         "stmf_attempt": [_vp, _int, _i64, _i64, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_int)],
         "stmf_bench_product": [_vp, _int, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)],
         "stmf_trop_matmul": [_int, _i64, _int, _i64, _vp, _vp, _vp, _vp, _int],
+        "stmf_stream": [_vp, ctypes.POINTER(_vp)],
+        "stmf_set_profiling": [_vp, _int],
+        "stmf_counters": [_vp, _vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -103,7 +106,8 @@ def lib():
 EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_destroy", "stmf_info",
                     "stmf_set_factors", "stmf_get_factors", "stmf_objective", "stmf_run",
                     "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
-                    "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul"]
+                    "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
+                    "stmf_stream", "stmf_set_profiling", "stmf_counters"]
 
 
 def _check(rc: int):
@@ -253,6 +257,22 @@ class Session:
         acc = _int()
         _check(lib().stmf_attempt(self._h, op, i, j, k, ctypes.byref(f), ctypes.byref(acc)))
         return f.value, bool(acc.value)
+
+    # measurement plumbing ----------------------------------------------------
+    def stream_handle(self) -> int:
+        h = _vp()
+        _check(lib().stmf_stream(self._h, ctypes.byref(h)))
+        return int(h.value or 0)
+
+    def set_profiling(self, on: bool = True):
+        _check(lib().stmf_set_profiling(self._h, int(on)))
+
+    def counters(self) -> dict:
+        c = np.zeros(8, np.int64)
+        _check(lib().stmf_counters(self._h, _p(c)))
+        keys = ("launches", "cub_sorts", "phaseB_launches", "phaseB_ns", "phaseB_timed",
+                "product_passes", "replicas", "given")
+        return dict(zip(keys, (int(x) for x in c)))
 
     def bench_product(self, reps: int = 10, flush_l2: bool = True):
         ms = _dbl()

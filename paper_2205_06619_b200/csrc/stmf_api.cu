@@ -58,7 +58,15 @@ struct StmfError {
     }                                                                                        \
   } while (0)
 
-#define LAUNCH_CK() CK(cudaGetLastError())
+#include <atomic>
+// every kernel launch of this library is followed by LAUNCH_CK(): it also counts them
+static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_cub_calls{0};
+#define LAUNCH_CK()            \
+  do {                         \
+    g_launches++;              \
+    CK(cudaGetLastError());    \
+  } while (0)
 
 [[noreturn]] static void fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -185,6 +193,9 @@ struct SessionBase {
   virtual void try_update(int op, int64_t i, int64_t j, int k, void* ucol, void* vrow, double* f,
                           bool commit, int* accepted) = 0;
   virtual void bench_product(int reps, int flush, double* ms, double* err) = 0;
+  virtual void* stream() = 0;
+  virtual void set_profiling(int on) = 0;
+  virtual void counters(int64_t* out) = 0;
 };
 
 template <typename T>
@@ -254,9 +265,28 @@ struct Session : SessionBase {
   bool err_valid = false;
   double err = 0;
   int64_t n_product_passes = 0, n_escalations = 0;
+  bool profiling = false;
+  cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr;
+  long long phaseB_launches = 0, phaseB_ns = 0, phaseB_timed = 0;
+
+  void* stream() override { return (void*)st; }
+  void set_profiling(int on) override {
+    if (on && !ev_b0) {
+      CK(cudaEventCreate(&ev_b0));
+      CK(cudaEventCreate(&ev_b1));
+    }
+    profiling = on != 0;
+  }
+  void counters(int64_t* out) override {
+    out[0] = g_launches.load(); out[1] = g_cub_calls.load(); out[2] = phaseB_launches;
+    out[3] = phaseB_ns; out[4] = phaseB_timed; out[5] = n_product_passes; out[6] = n_escalations;
+    out[7] = N;
+  }
   std::vector<int> batch_sched;
 
   ~Session() override {
+    if (ev_b0) cudaEventDestroy(ev_b0);
+    if (ev_b1) cudaEventDestroy(ev_b1);
     if (h_acc) cudaFreeHost(h_acc);
     if (h_chg) cudaFreeHost(h_chg);
     if (h_flags) cudaFreeHost(h_flags);
@@ -448,8 +478,8 @@ struct Session : SessionBase {
                                                                 t1c.p, t2c.p, agc.p, score.p, colhist.p,
                                                                 exact_limit, flags.p);
       } else {
-        k_product_csc_seq<T><<<nblk(n, 64), 64, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p, t1c.p,
-                                                          t2c.p, agc.p, score.p, colhist.p);
+        k_product_csc_warpseq<T><<<warps_grid(n), 256, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p,
+                                                                  t1c.p, t2c.p, agc.p, score.p, colhist.p);
         LAUNCH_CK();
         if (n == 1) {
           DevBuf<double> col;
@@ -502,8 +532,10 @@ struct Session : SessionBase {
     size_t bytes = cubtmp_bytes;
     // residuals are >= 0: bits 63 is clear, sort on bits 0..62
     CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res.p, res_sorted.p, (int64_t)N, 0, 63, st));
+    g_cub_calls++;
     int nl = (int)pw.loff.size();
-    k_pw_leaves<<<nblk(nl, 128), 128, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, res_sorted.p, pwval.p);
+    k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, res_sorted.p,
+                                                            pwval.p);
     LAUNCH_CK();
     if (pw.H > 0) {
       k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, pwval.p);
@@ -531,6 +563,7 @@ struct Session : SessionBase {
     LAUNCH_CK();
     size_t bytes = cubtmp_bytes;
     CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, bytes, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)nc, 0, 64, st));
+    g_cub_calls++;
     unsigned nb = std::max(1u, std::min(nblk(nc, 256), 64u));
     k_cand_build<T><<<nb, 256, sizeof(int32_t) * rank, st>>>(nc, rank, col_idx.p + beg, xr.p + beg, agr.p + beg,
                                                              cperm.p, colhist.p, cj.p, ck.p, cx.p);
@@ -570,17 +603,22 @@ struct Session : SessionBase {
     LAUNCH_CK();
     constexpr int EG = 8;
     int ng = (E + EG - 1) / EG;
-    k_phaseB<T, EG><<<warps_grid(m * ng), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, E, bk,
-                                                         vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf, flags.p, F,
-                                                         exact_limit);
+    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, (int)n, Ut.p, ubufB.p, acc_ulf, chg_ulf};
+    SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, (int)m, V.p, vbufB.p, acc_urf, chg_urf};
+    if (profiling) CK(cudaEventRecord(ev_b0, st));
+    k_phaseB<T, EG><<<warps_grid((m + n) * ng), 256, 0, st>>>(sa, sb, E, bk, flags.p, F, exact_limit);
     LAUNCH_CK();
-    k_phaseB<T, EG><<<warps_grid(n * ng), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, E, bk,
-                                                         ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf, flags.p, F,
-                                                         exact_limit);
-    LAUNCH_CK();
+    if (profiling) CK(cudaEventRecord(ev_b1, st));
+    phaseB_launches++;
     CK(cudaMemcpyAsync(h_acc, acc.p, sizeof(u64) * 4 * E, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_chg, chg.p, sizeof(int) * 2 * E, cudaMemcpyDeviceToHost, st));
     check_flags();
+    if (profiling) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev_b0, ev_b1));
+      phaseB_ns += (long long)(ms * 1e6);
+      phaseB_timed++;
+    }
   }
 
   const T* eval_a(int op, int q) const { return op == 0 ? ubufB.p + (size_t)q * m : ubufA.p + (size_t)q * m; }
@@ -956,6 +994,21 @@ int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, c
   if (dtype == STMF_F64) { GUARD(trop_matmul_impl<double>(m, rank, n, U, V, P, arg, device)); }
   if (dtype == STMF_F32) { GUARD(trop_matmul_impl<float>(m, rank, n, U, V, P, arg, device)); }
   return set_err(STMF_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+int stmf_stream(stmf_session* s, void** stream) {
+  NEED(s);
+  GUARD(*stream = s->impl->stream());
+}
+
+int stmf_set_profiling(stmf_session* s, int on) {
+  NEED(s);
+  GUARD(s->impl->set_profiling(on));
+}
+
+int stmf_counters(stmf_session* s, int64_t* out8) {
+  NEED(s);
+  GUARD(s->impl->counters(out8));
 }
 
 int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, double* err) {

@@ -209,6 +209,45 @@ __global__ void k_product_csc_seq(int64_t m, int64_t n, int rank, const int64_t*
   score[c] = s;
 }
 
+// CSC pass, fp64 oracle-compat, warp per column: lanes compute 32 entries'
+// products in parallel, then every lane folds the 32 td values in row order with
+// shuffles — the same sequential summation order as k_product_csc_seq.  The TD_A
+// histogram is counted in a per-warp shared-memory slice (rank <= 255).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_product_csc_warpseq(int64_t m, int64_t n, int rank, const int64_t* __restrict__ ptr,
+                      const int32_t* __restrict__ idx, const T* __restrict__ xc, const T* __restrict__ Ut,
+                      const T* __restrict__ V, T* __restrict__ t1, T* __restrict__ t2, uint8_t* __restrict__ ag,
+                      double* __restrict__ score, int32_t* __restrict__ colhist) {
+  __shared__ int32_t hist[8][256];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w; c < n; c += nw) {
+    for (int l = lane; l < rank; l += 32) hist[wib][l] = 0;
+    __syncwarp();
+    double s = 0.0;
+    int64_t beg = ptr[c], end = ptr[c + 1];
+    for (int64_t base = beg; base < end; base += 32) {
+      int64_t p = base + lane;
+      double td = 0.0;
+      if (p < end) {
+        T b1, b2; int a;
+        top2_entry(Ut, V, m, n, rank, (int64_t)idx[p], c, b1, b2, a);
+        t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a;
+        td = (double)vabs(sub_rn(xc[p], b1));
+        atomicAdd(&hist[wib][a], 1);
+      }
+      int cnt = end - base < 32 ? (int)(end - base) : 32;
+      for (int l = 0; l < cnt; l++) s = __dadd_rn(s, __shfl_sync(0xffffffffu, td, l));
+    }
+    __syncwarp();
+    if (lane == 0) score[c] = s;
+    for (int l = lane; l < rank; l += 32) colhist[c * rank + l] = hist[wib][l];
+    __syncwarp();
+  }
+}
+
 // CSC pass, exact mode: warp per column; the fp64 partials of binary32 terms on
 // the 2^-g grid are exact below 2^(53-g) (checked: flag bit 4), so the warp sum
 // is the exact column score, order independent.
@@ -427,82 +466,110 @@ __global__ void k_chk_vec(int64_t len, int E, const int32_t* __restrict__ ck, co
 // over the line: sum_p |x_p - max(Q^k_p, w_q + vin_q[idx_p])| with
 // Q^k_p = (ag_p == k) ? t2_p : t1_p  (U(x)V with column/row k replaced).
 // The line partial (fp64) goes to a 128-bit fixed-point accumulator per eval.
+template <typename T>
+struct SideB {
+  int64_t nlines;
+  const int64_t* ptr;
+  const int32_t* idx;
+  const T* xv;
+  const T* t1;
+  const T* t2;
+  const uint8_t* ag;
+  const T* vin;      // E x len_other: the eval's first-residuation vector
+  int len_other;
+  const T* cur;      // rank x nlines: current factor row for this side
+  T* out;            // E x nlines: second residuation
+  u64* acc;          // 2 per eval
+  int* chg;          // 1 per eval
+};
+
+template <int EG, typename V>
+__device__ __forceinline__ V lane_pick(const V (&a)[EG], int q) {
+  V v = a[0];
+#pragma unroll
+  for (int i = 1; i < EG; i++)
+    if (q == i) v = a[i];
+  return v;
+}
+
+template <typename T, int EG>
+__device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E, const int32_t* __restrict__ ek,
+                                            int lane, int* __restrict__ flags, int F, double exact_limit) {
+  int64_t nlines = S.nlines;
+  int g = (int)(it / nlines);  // group-major: concurrent warps share the same vin rows
+  int64_t L = it - (int64_t)g * nlines;
+  int e0 = g * EG;
+  int ne = E - e0 < EG ? E - e0 : EG;
+  const T* __restrict__ vbase = S.vin + (int64_t)e0 * S.len_other;
+  int qoff[EG], kq[EG];
+#pragma unroll
+  for (int q = 0; q < EG; q++) {
+    int qq = q < ne ? q : ne - 1;
+    qoff[q] = qq * S.len_other;
+    kq[q] = ek[e0 + qq];
+  }
+  int64_t beg = S.ptr[L], end = S.ptr[L + 1];
+  T mn[EG];
+#pragma unroll
+  for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
+  for (int64_t p = beg + lane; p < end; p += 32) {
+    T x = S.xv[p];
+    int c = S.idx[p];
+#pragma unroll
+    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, __ldg(vbase + qoff[q] + c)));
+  }
+#pragma unroll
+  for (int q = 0; q < EG; q++)
+    for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
+  if (lane < ne) {
+    T w = lane_pick<EG>(mn, lane);
+    int kl = lane_pick<EG>(kq, lane);
+    S.out[(int64_t)(e0 + lane) * nlines + L] = w;
+    if (w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
+  }
+  double part[EG];
+#pragma unroll
+  for (int q = 0; q < EG; q++) part[q] = 0.0;
+  for (int64_t p = beg + lane; p < end; p += 32) {
+    T x = S.xv[p];
+    int c = S.idx[p];
+    T a1 = S.t1[p], a2 = S.t2[p];
+    int a = S.ag[p];
+#pragma unroll
+    for (int q = 0; q < EG; q++) {
+      T Q = (a == kq[q]) ? a2 : a1;
+      T pm = vmax(Q, add_rn(mn[q], __ldg(vbase + qoff[q] + c)));
+      part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < EG; q++)
+    for (int o = 16; o; o >>= 1) part[q] = __dadd_rn(part[q], shfl_xor(part[q], o));
+  if (lane < ne) {
+    double pv = lane_pick<EG>(part, lane);
+    int fl = 0;
+    if (!(pv < exact_limit)) fl |= 4;
+    u64 hi, lo;
+    fx_from_double(pv, F, hi, lo, fl);
+    fx_atomic_add(S.acc + 2 * (e0 + lane), hi, lo);
+    if (fl & 6) atomicOr(flags, fl);
+  }
+}
+
+// Phase B of both update rules in one launch: items [0, A) are F-ULF evals on CSR
+// rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
 template <typename T, int EG>
 __global__ void __launch_bounds__(256)
-k_phaseB(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-         const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
-         const uint8_t* __restrict__ ag, int E, const int32_t* __restrict__ ek, const T* __restrict__ vin,
-         int64_t len_other, const T* __restrict__ cur, T* __restrict__ out, u64* __restrict__ acc,
-         int* __restrict__ chg, int* __restrict__ flags, int F, double exact_limit) {
+k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
+         double exact_limit) {
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int ngroups = (E + EG - 1) / EG;
-  int64_t items = nlines * ngroups;
+  int64_t itemsA = A.nlines * ngroups, items = itemsA + B.nlines * ngroups;
   for (int64_t it = w; it < items; it += nw) {
-    int g = (int)(it / nlines);  // group-major: concurrent warps share the same vin rows
-    int64_t L = it - (int64_t)g * nlines;
-    int e0 = g * EG;
-    int ne = E - e0 < EG ? E - e0 : EG;
-    const T* vq[EG];
-    int kq[EG];
-#pragma unroll
-    for (int q = 0; q < EG; q++) {
-      int e = e0 + (q < ne ? q : 0);
-      vq[q] = vin + (int64_t)e * len_other;
-      kq[q] = ek[e];
-    }
-    int64_t beg = ptr[L], end = ptr[L + 1];
-    T mn[EG];
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-    for (int64_t p = beg + lane; p < end; p += 32) {
-      T x = xv[p];
-      int c = idx[p];
-#pragma unroll
-      for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, __ldg(vq[q] + c)));
-    }
-#pragma unroll
-    for (int q = 0; q < EG; q++)
-      for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < EG; q++)
-        if (q < ne) {
-          out[(int64_t)(e0 + q) * nlines + L] = mn[q];
-          if (mn[q] != cur[(int64_t)kq[q] * nlines + L]) chg[e0 + q] = 1;
-        }
-    }
-    double part[EG];
-#pragma unroll
-    for (int q = 0; q < EG; q++) part[q] = 0.0;
-    for (int64_t p = beg + lane; p < end; p += 32) {
-      T x = xv[p];
-      int c = idx[p];
-      T a1 = t1[p], a2 = t2[p];
-      int a = ag[p];
-#pragma unroll
-      for (int q = 0; q < EG; q++) {
-        T Q = (a == kq[q]) ? a2 : a1;
-        T pm = vmax(Q, add_rn(mn[q], __ldg(vq[q] + c)));
-        part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < EG; q++)
-      for (int o = 16; o; o >>= 1) part[q] = __dadd_rn(part[q], shfl_xor(part[q], o));
-    if (lane == 0) {
-      int fl = 0;
-#pragma unroll
-      for (int q = 0; q < EG; q++)
-        if (q < ne) {
-          if (!(part[q] < exact_limit)) fl |= 4;
-          u64 hi, lo;
-          fx_from_double(part[q], F, hi, lo, fl);
-          fx_atomic_add(acc + 2 * (e0 + q), hi, lo);
-        }
-      if (fl) atomicOr(flags, fl);
-    }
+    if (it < itemsA) phaseB_item<T, EG>(A, it, E, ek, lane, flags, F, exact_limit);
+    else phaseB_item<T, EG>(B, it - itemsA, E, ek, lane, flags, F, exact_limit);
   }
 }
 
@@ -581,6 +648,45 @@ __global__ void k_pw_leaves(int nleaves, const int64_t* __restrict__ loff, const
     for (; i < n; i++) res = __dadd_rn(res, a[i]);
   }
   val[lnode[t]] = res;
+}
+
+// Same leaves, 8 lanes per leaf (4 leaves per warp): lane j of a group owns
+// numpy's accumulator r[j] (elements j, j+8, ...), so every add happens in the
+// same order as numpy's; the 3-level combine and the tail run on lane 0.
+__global__ void k_pw_leaves8(int nleaves, const int64_t* __restrict__ loff, const int32_t* __restrict__ llen,
+                             const int32_t* __restrict__ lnode, const u64* __restrict__ sorted,
+                             double* __restrict__ val) {
+  int lane = threadIdx.x & 31;
+  int j = lane & 7;
+  int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3);
+  bool ok = t < nleaves;
+  const double* a = reinterpret_cast<const double*>(sorted) + (ok ? loff[t] : 0);
+  int n = ok ? llen[t] : 0;
+  double r = 0.0;
+  int body = n - (n % 8);
+  if (n >= 8) {
+    r = a[j];
+    for (int i = 8 + j; i < body; i += 8) r = __dadd_rn(r, a[i]);
+  }
+  // gather the 8 accumulators of this group into lane j == 0
+  double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+  double r2 = __shfl_down_sync(0xffffffffu, r, 2);
+  double r3 = __shfl_down_sync(0xffffffffu, r, 3);
+  double r4 = __shfl_down_sync(0xffffffffu, r, 4);
+  double r5 = __shfl_down_sync(0xffffffffu, r, 5);
+  double r6 = __shfl_down_sync(0xffffffffu, r, 6);
+  double r7 = __shfl_down_sync(0xffffffffu, r, 7);
+  if (ok && j == 0) {
+    double res;
+    if (n < 8) {
+      res = 0.0;
+      for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    } else {
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r, r1), __dadd_rn(r2, r3)), __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+      for (int i = body; i < n; i++) res = __dadd_rn(res, a[i]);
+    }
+    val[lnode[t]] = res;
+  }
 }
 
 // numpy replica, step 4: combine internal nodes level by level (heights 1..H).
