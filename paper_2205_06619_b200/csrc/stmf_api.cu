@@ -241,14 +241,17 @@ struct Session : SessionBase {
   DevBuf<T> cx, xrow_dense;
   // batch scratch
   int Emax = 512;
-  DevBuf<T> vbuf, ubufB, ubufA, vbufB;
+  DevBuf<T> vbuf, ubufB, ubufA, vbufB, dtmpA, dtmpB;
   DevBuf<u64> acc;
   DevBuf<int> chg, flags, findpos;
   u64* h_acc = nullptr;
   int* h_chg = nullptr;
   int* h_flags = nullptr;
   // replica
-  DevBuf<u64> res, res_sorted;
+  DevBuf<u64> res, res_sorted, res_cur, S_cur, dolds, dnews;
+  DevBuf<int> dcount;
+  bool cur_valid = false;
+  int64_t n_delta_replicas = 0;
   DevBuf<double> pwval;
   DevBuf<int64_t> pw_loff;
   DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
@@ -306,13 +309,13 @@ struct Session : SessionBase {
     CK(cudaGetDeviceProperties(&prop, dev));
     nsm = prop.multiProcessorCount;
     if (const char* e = getenv("STMF_EMAX")) Emax = std::max(8, atoi(e));
-    batch_sched = {8, 32, 128, 512};
+    Emax = (Emax + kEG - 1) / kEG * kEG;
+    batch_sched.clear();  // filled once N is known (see below)
     if (const char* e = getenv("STMF_BATCH")) {
       batch_sched.clear();
       const char* p = e;
       while (*p) { batch_sched.push_back(std::max(1, atoi(p))); while (*p && *p != ',') p++; if (*p) p++; }
     }
-    for (int& b : batch_sched) b = std::min(b, Emax);
     // upload dense X + mask, build CSR/CSC, free the dense copies
     DevBuf<T> dX;
     DevBuf<uint8_t> dM;
@@ -343,6 +346,15 @@ struct Session : SessionBase {
       if (c == 0) fail(STMF_ERR_INVALID, "column %lld has no given entries", (long long)j);
       max_colnnz = std::max(max_colnnz, c);
     }
+    if (batch_sched.empty()) {
+      // speculative batch sizes (candidates): the first batch balances the fixed
+      // per-batch cost (~40 us of launches + one host sync) against the cost of an
+      // evaluation (~N given entries); later batches grow 4x (a stuck row needs all).
+      int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
+      for (int b = b0; b < Emax; b *= 4) batch_sched.push_back(b);
+      batch_sched.push_back(Emax);
+    }
+    for (int& b : batch_sched) b = std::max(1, std::min(b, Emax));
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
@@ -363,14 +375,17 @@ struct Session : SessionBase {
     cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
     vbuf.alloc((size_t)Emax * n); ubufB.alloc((size_t)Emax * m);
     ubufA.alloc((size_t)Emax * m); vbufB.alloc((size_t)Emax * n);
+    dtmpA.alloc(m); dtmpB.alloc(n);
     acc.alloc(4 * (size_t)Emax); chg.alloc(2 * (size_t)Emax); flags.alloc(4); findpos.alloc(2);
     CK(cudaMallocHost(&h_acc, sizeof(u64) * 4 * Emax));
     CK(cudaMallocHost(&h_chg, sizeof(int) * 2 * Emax));
     CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
+    h_flags[0] = h_flags[1] = 0;
     size_t b1 = 0, b2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)n, 0, 64, st));
     if (!kExact) {
-      res.alloc(N); res_sorted.alloc(N);
+      res.alloc(N); res_sorted.alloc(N); res_cur.alloc(N); S_cur.alloc(N);
+      dolds.alloc(kDeltaCap); dnews.alloc(kDeltaCap); dcount.alloc(1);
       CK(cub::DeviceRadixSort::SortKeys(nullptr, b2, res.p, res_sorted.p, (int64_t)N, 0, 64, st));
       pw.build(N);
       pwval.alloc(pw.nnodes);
@@ -432,6 +447,7 @@ struct Session : SessionBase {
     }
     CK(cudaStreamSynchronize(st));
     have_factors = true;
+    cur_valid = false;
     dirty = true;
     stats_dirty.assign(rank, 1);
     err_valid = false;
@@ -526,13 +542,37 @@ struct Session : SessionBase {
   // numpy replica: np.sum(np.sort(|residuals|)) bit for bit (tropical.py:211)
   double replica(int k, const T* a, const T* b) {
     n_escalations++;
-    k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k, a, b,
-                                                    res.p);
-    LAUNCH_CK();
-    size_t bytes = cubtmp_bytes;
-    // residuals are >= 0: bits 63 is clear, sort on bits 0..62
-    CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res.p, res_sorted.p, (int64_t)N, 0, 63, st));
-    g_cub_calls++;
+    bool full = !cur_valid;
+    if (!full) {
+      CK(cudaMemsetAsync(dcount.p, 0, sizeof(int), st));
+      k_residuals_delta<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k,
+                                                            a, b, res_cur.p, res.p, dolds.p, dnews.p, dcount.p);
+      LAUNCH_CK();
+      CK(cudaMemcpyAsync(h_flags + 1, dcount.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      int D = h_flags[1];
+      if (D > kDeltaCap) {
+        full = true;
+      } else {
+        n_delta_replicas++;
+        if (D > 0) {
+          k_sort_delta<<<2, 1024, 0, st>>>(dolds.p, dnews.p, dcount.p);
+          LAUNCH_CK();
+        }
+        k_merge_delta<<<nblk(N + D, 256), 256, 0, st>>>(N, S_cur.p, dolds.p, dnews.p, dcount.p, res_sorted.p);
+        LAUNCH_CK();
+      }
+    } else {
+      k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k, a, b,
+                                                      res.p);
+      LAUNCH_CK();
+    }
+    if (full) {
+      size_t bytes = cubtmp_bytes;
+      // residuals are >= 0: bit 63 is clear, sort on bits 0..62
+      CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res.p, res_sorted.p, (int64_t)N, 0, 63, st));
+      g_cub_calls++;
+    }
     int nl = (int)pw.loff.size();
     k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, res_sorted.p,
                                                             pwval.p);
@@ -547,10 +587,18 @@ struct Session : SessionBase {
     return v;
   }
 
+  // the last replica's arrays (res, res_sorted) become the current state's
+  void adopt_replica() {
+    std::swap(res_cur.p, res.p);
+    std::swap(S_cur.p, res_sorted.p);
+    cur_valid = true;
+  }
+
   double objective() override {
     ensure_caches();
     if (!err_valid) {
       err = state_objective(0, Ut.p, V.p);
+      if (!kExact) adopt_replica();
       err_valid = true;
     }
     return err;
@@ -592,21 +640,21 @@ struct Session : SessionBase {
     CK(cudaMemsetAsync(acc.p, 0, sizeof(u64) * 4 * E, st));
     CK(cudaMemsetAsync(chg.p, 0, sizeof(int) * 2 * E, st));
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
-    k_phaseA_ulf<T><<<nblk((int64_t)E * n, 256), 256, 0, st>>>(n, E, i, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
-                                                                  xrow_dense.p, vbuf.p, chg_ulf);
+    int64_t G8 = (int64_t)((E + kEG - 1) / kEG) * kEG;
+    k_phaseA_ulf<T><<<nblk(G8 * n, 256), 256, 0, st>>>(n, E, i, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
+                                                        xrow_dense.p, vbuf.p, chg_ulf);
     LAUNCH_CK();
-    k_phaseA_urf_fill<T><<<nblk((int64_t)E * m, 256), 256, 0, st>>>(m, E, bj, bk, rm1.p, rm2.p, rmarg.p, ubufA.p);
+    k_phaseA_urf_fill<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bj, bk, rm1.p, rm2.p, rmarg.p, ubufA.p);
     LAUNCH_CK();
     k_phaseA_urf_seed<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p);
     LAUNCH_CK();
-    k_chk_vec<T><<<nblk((int64_t)E * m, 256), 256, 0, st>>>(m, E, bk, ubufA.p, Ut.p, chg_urf);
+    k_chk_ilv<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bk, ubufA.p, Ut.p, chg_urf);
     LAUNCH_CK();
-    constexpr int EG = 8;
-    int ng = (E + EG - 1) / EG;
-    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, (int)n, Ut.p, ubufB.p, acc_ulf, chg_ulf};
-    SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, (int)m, V.p, vbufB.p, acc_urf, chg_urf};
+    int ng = (E + kEG - 1) / kEG;
+    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf};
+    SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
-    k_phaseB<T, EG><<<warps_grid((m + n) * ng), 256, 0, st>>>(sa, sb, E, bk, flags.p, F, exact_limit);
+    k_phaseB<T><<<warps_grid((m + n) * ng), 256, 0, st>>>(sa, sb, E, bk, flags.p, F, exact_limit);
     LAUNCH_CK();
     if (profiling) CK(cudaEventRecord(ev_b1, st));
     phaseB_launches++;
@@ -621,8 +669,19 @@ struct Session : SessionBase {
     }
   }
 
-  const T* eval_a(int op, int q) const { return op == 0 ? ubufB.p + (size_t)q * m : ubufA.p + (size_t)q * m; }
-  const T* eval_b(int op, int q) const { return op == 0 ? vbuf.p + (size_t)q * n : vbufB.p + (size_t)q * n; }
+  // final column k of U (a) and row k of V (b) of eval (op, q) of the last batch
+  const T* eval_a(int op, int q) {
+    if (op == 0) return ubufB.p + (size_t)q * m;
+    k_deinterleave<T><<<nblk(m, 256), 256, 0, st>>>(m, q, ubufA.p, dtmpA.p);
+    LAUNCH_CK();
+    return dtmpA.p;
+  }
+  const T* eval_b(int op, int q) {
+    if (op == 1) return vbufB.p + (size_t)q * n;
+    k_deinterleave<T><<<nblk(n, 256), 256, 0, st>>>(n, q, vbuf.p, dtmpB.p);
+    LAUNCH_CK();
+    return dtmpB.p;
+  }
 
   // decide eval (op, q) of the current batch against err; returns 1 = accept (f set)
   int decide(int op, int q, int E, int k, double* f) {
@@ -647,7 +706,9 @@ struct Session : SessionBase {
     return fr < err;
   }
 
+  // accept eval (op, q); in fp64 mode its replica was the last one computed
   void commit(int op, int q, int k) {
+    if (!kExact) adopt_replica();
     CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, eval_a(op, q), sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(V.p + (size_t)k * n, eval_b(op, q), sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
     dirty = true;

@@ -397,23 +397,56 @@ __global__ void k_scatter_row(int64_t nc, const int32_t* __restrict__ cols, cons
 }
 
 // ----------------------------------------------------------------------------
+// Phase A writes each eval's first-residuation vector in a planar eval-interleaved
+// layout  I[g][p][line][EGP]  (g = group of kEG evals, p = plane of EGP = 16 bytes
+// of evals): phase B fetches the kEG values of one given entry with kEG/EGP 16-byte
+// loads, and the 32 lanes of each load read consecutive 16-byte slots (few L1
+// wavefronts) instead of kEG scattered gathers.
+constexpr int kEG = 8;
+
+template <typename T>
+struct Ilv {
+  static constexpr int EGP = 16 / (int)sizeof(T);
+  static constexpr int P = kEG / EGP;
+};
+
+template <typename T>
+__device__ __forceinline__ int64_t ilv_index(int q, int64_t a, int64_t len) {
+  constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
+  int g = q / kEG, p = (q % kEG) / EGP, e = q % EGP;
+  return (((int64_t)g * P + p) * len + a) * EGP + e;
+}
+
+template <typename T>
+__device__ __forceinline__ void ilv_decode(int64_t t, int64_t len, int& q, int64_t& a) {
+  constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
+  int e = (int)(t % EGP);
+  int64_t rest = t / EGP;
+  a = rest % len;
+  int64_t gp = rest / len;
+  q = (int)(gp / P) * kEG + (int)(gp % P) * EGP + e;
+}
+
 // Phase A.  F-ULF evals q: v'_c = min(CM^(-i)_c, X_ic - s_q), s_q = X_ij - V_kj
 // (engine.py:222-223: U_ik <- X_ij - V_kj; V_k. <- rr(U_.k), with only u_i changed).
 template <typename T>
 __global__ void k_phaseA_ulf(int64_t n, int E, int64_t i, const int32_t* __restrict__ cj,
                              const int32_t* __restrict__ ck, const T* __restrict__ cx, const T* __restrict__ V,
                              const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
-                             const T* __restrict__ xrow_dense, T* __restrict__ vbuf, int* __restrict__ chg) {
+                             const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)E * n) return;
-  int q = (int)(t / n);
-  int64_t c = t - (int64_t)q * n;
+  int G = (E + kEG - 1) / kEG;
+  if (t >= (int64_t)G * kEG * n) return;
+  int q;
+  int64_t c;
+  ilv_decode<T>(t, n, q, c);
+  if (q >= E) { vI[t] = tinf<T>(); return; }
   int k = ck[q];
   int64_t kn = (int64_t)k * n;
   T s = sub_rn(cx[q], V[kn + cj[q]]);
   T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
   T v = vmin(cmx, sub_rn(xrow_dense[c], s));
-  vbuf[(int64_t)q * n + c] = v;
+  vI[t] = v;
   if (v != V[kn + c]) chg[q] = 1;
 }
 
@@ -422,13 +455,16 @@ __global__ void k_phaseA_ulf(int64_t n, int E, int64_t i, const int32_t* __restr
 template <typename T>
 __global__ void k_phaseA_urf_fill(int64_t m, int E, const int32_t* __restrict__ cj, const int32_t* __restrict__ ck,
                                   const T* __restrict__ rm1, const T* __restrict__ rm2,
-                                  const int32_t* __restrict__ rmarg, T* __restrict__ ubuf) {
+                                  const int32_t* __restrict__ rmarg, T* __restrict__ uI) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)E * m) return;
-  int q = (int)(t / m);
-  int64_t r = t - (int64_t)q * m;
+  int G = (E + kEG - 1) / kEG;
+  if (t >= (int64_t)G * kEG * m) return;
+  int q;
+  int64_t r;
+  ilv_decode<T>(t, m, q, r);
+  if (q >= E) { uI[t] = tinf<T>(); return; }
   int64_t km = (int64_t)ck[q] * m;
-  ubuf[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+  uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
 }
 
 template <typename T>
@@ -436,31 +472,41 @@ __global__ void k_phaseA_urf_seed(int64_t m, int E, int64_t i, const int32_t* __
                                   const int32_t* __restrict__ ck, const T* __restrict__ cx,
                                   const T* __restrict__ Ut, const int64_t* __restrict__ col_ptr,
                                   const int32_t* __restrict__ row_idx, const T* __restrict__ xc,
-                                  T* __restrict__ ubuf) {
+                                  T* __restrict__ uI) {
   int q = blockIdx.x;
   if (q >= E) return;
   int j = cj[q];
   int64_t km = (int64_t)ck[q] * m;
   T s = sub_rn(cx[q], Ut[km + i]);
-  T* u = ubuf + (int64_t)q * m;
+  T* u = uI + ilv_index<T>(q, 0, m);
   for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
-    int r = row_idx[p];
+    int64_t r = row_idx[p] * Ilv<T>::EGP;
     u[r] = vmin(u[r], sub_rn(xc[p], s));
   }
 }
 
+// change flag of an interleaved vector against the current factor row
 template <typename T>
-__global__ void k_chk_vec(int64_t len, int E, const int32_t* __restrict__ ck, const T* __restrict__ buf,
+__global__ void k_chk_ilv(int64_t len, int E, const int32_t* __restrict__ ck, const T* __restrict__ I,
                           const T* __restrict__ cur, int* __restrict__ chg) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)E * len) return;
-  int q = (int)(t / len);
-  int64_t a = t - (int64_t)q * len;
-  if (buf[t] != cur[(int64_t)ck[q] * len + a]) chg[q] = 1;
+  int G = (E + kEG - 1) / kEG;
+  if (t >= (int64_t)G * kEG * len) return;
+  int q;
+  int64_t a;
+  ilv_decode<T>(t, len, q, a);
+  if (q < E && I[t] != cur[(int64_t)ck[q] * len + a]) chg[q] = 1;
+}
+
+// eval q of an interleaved buffer -> contiguous vector
+template <typename T>
+__global__ void k_deinterleave(int64_t len, int q, const T* __restrict__ I, T* __restrict__ out) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < len) out[a] = I[ilv_index<T>(q, a, len)];
 }
 
 // ----------------------------------------------------------------------------
-// Phase B — the hot kernel.  Work item = (line L, group of EG evals).  For each
+// Phase B — the hot kernel.  Work item = (line L, group of kEG evals).  For each
 // eval q: line value w_q = min_p (x_p - vin_q[idx_p])  (the second residuation:
 // rc for F-ULF on CSR rows, rr for F-URF on CSC columns), then the eval's error
 // over the line: sum_p |x_p - max(Q^k_p, w_q + vin_q[idx_p])| with
@@ -475,8 +521,8 @@ struct SideB {
   const T* t1;
   const T* t2;
   const uint8_t* ag;
-  const T* vin;      // E x len_other: the eval's first-residuation vector
-  int len_other;
+  const T* vin;      // planar interleaved [g][p][len_other][EGP]: first-residuation vectors
+  int64_t len_other;
   const T* cur;      // rank x nlines: current factor row for this side
   T* out;            // E x nlines: second residuation
   u64* acc;          // 2 per eval
@@ -492,31 +538,46 @@ __device__ __forceinline__ V lane_pick(const V (&a)[EG], int q) {
   return v;
 }
 
-template <typename T, int EG>
+// the kEG values of entry column c of one group (group base g, plane stride len)
+__device__ __forceinline__ void load_eg(const float* __restrict__ g, int64_t len, int64_t c, float (&v)[kEG]) {
+  float4 a = __ldg(reinterpret_cast<const float4*>(g) + c);
+  float4 b = __ldg(reinterpret_cast<const float4*>(g) + len + c);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load_eg(const double* __restrict__ g, int64_t len, int64_t c, double (&v)[kEG]) {
+#pragma unroll
+  for (int i = 0; i < kEG / 2; i++) {
+    double2 a = __ldg(reinterpret_cast<const double2*>(g) + i * len + c);
+    v[2 * i] = a.x; v[2 * i + 1] = a.y;
+  }
+}
+
+template <typename T>
 __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E, const int32_t* __restrict__ ek,
                                             int lane, int* __restrict__ flags, int F, double exact_limit) {
+  constexpr int EG = kEG;
   int64_t nlines = S.nlines;
-  int g = (int)(it / nlines);  // group-major: concurrent warps share the same vin rows
-  int64_t L = it - (int64_t)g * nlines;
+  int ngroups = (E + EG - 1) / EG;
+  // line-major: the warps of one line (one per eval group) run together, so the
+  // line's entries are read from DRAM once per batch; the small vin blocks stay in L2
+  int64_t L = it / ngroups;
+  int g = (int)(it - L * ngroups);
   int e0 = g * EG;
   int ne = E - e0 < EG ? E - e0 : EG;
-  const T* __restrict__ vbase = S.vin + (int64_t)e0 * S.len_other;
-  int qoff[EG], kq[EG];
+  const T* __restrict__ vg = S.vin + (int64_t)g * S.len_other * EG;
+  int kq[EG];
 #pragma unroll
-  for (int q = 0; q < EG; q++) {
-    int qq = q < ne ? q : ne - 1;
-    qoff[q] = qq * S.len_other;
-    kq[q] = ek[e0 + qq];
-  }
+  for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
   int64_t beg = S.ptr[L], end = S.ptr[L + 1];
   T mn[EG];
 #pragma unroll
   for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
   for (int64_t p = beg + lane; p < end; p += 32) {
     T x = S.xv[p];
-    int c = S.idx[p];
+    T v[EG];
+    load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
 #pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, __ldg(vbase + qoff[q] + c)));
+    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
   }
 #pragma unroll
   for (int q = 0; q < EG; q++)
@@ -532,13 +593,14 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   for (int q = 0; q < EG; q++) part[q] = 0.0;
   for (int64_t p = beg + lane; p < end; p += 32) {
     T x = S.xv[p];
-    int c = S.idx[p];
     T a1 = S.t1[p], a2 = S.t2[p];
     int a = S.ag[p];
+    T v[EG];
+    load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
 #pragma unroll
     for (int q = 0; q < EG; q++) {
       T Q = (a == kq[q]) ? a2 : a1;
-      T pm = vmax(Q, add_rn(mn[q], __ldg(vbase + qoff[q] + c)));
+      T pm = vmax(Q, add_rn(mn[q], v[q]));
       part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
     }
   }
@@ -558,18 +620,18 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
 
 // Phase B of both update rules in one launch: items [0, A) are F-ULF evals on CSR
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
-template <typename T, int EG>
-__global__ void __launch_bounds__(256)
+template <typename T>
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 4)
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
          double exact_limit) {
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int ngroups = (E + EG - 1) / EG;
+  int ngroups = (E + kEG - 1) / kEG;
   int64_t itemsA = A.nlines * ngroups, items = itemsA + B.nlines * ngroups;
   for (int64_t it = w; it < items; it += nw) {
-    if (it < itemsA) phaseB_item<T, EG>(A, it, E, ek, lane, flags, F, exact_limit);
-    else phaseB_item<T, EG>(B, it - itemsA, E, ek, lane, flags, F, exact_limit);
+    if (it < itemsA) phaseB_item<T>(A, it, E, ek, lane, flags, F, exact_limit);
+    else phaseB_item<T>(B, it - itemsA, E, ek, lane, flags, F, exact_limit);
   }
 }
 
@@ -760,5 +822,109 @@ __global__ void k_colscore_single(int64_t m, const int64_t* __restrict__ ptr, co
   for (int64_t i = 0; i < m; i++) col[i] = 0.0;
   for (int64_t p = ptr[0]; p < ptr[1]; p++) col[idx[p]] = (double)vabs(sub_rn(xc[p], t1c[p]));
   score[0] = np_pairwise_dev(col, m);
+}
+}  // namespace stmf
+
+namespace stmf {
+// ----------------------------------------------------------------------------
+// Incremental numpy replica.  The current state's residuals (per given entry, CSR
+// order) and their ascending order S_cur are kept on the device.  A candidate's
+// sorted residual multiset = S_cur minus the old values of its changed entries
+// plus their new values; positions follow from binary searches (equal values are
+// interchangeable in the sum, so any tie order gives numpy's result).
+
+constexpr int kDeltaCap = 4096;
+
+// new residual bits of every entry; changed entries appended to (olds, news)
+template <typename T>
+__global__ void k_residuals_delta(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                  const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
+                                  const uint8_t* __restrict__ ag, int k, const T* __restrict__ a,
+                                  const T* __restrict__ b, const u64* __restrict__ res_cur, u64* __restrict__ out,
+                                  u64* __restrict__ olds, u64* __restrict__ news, int* __restrict__ dcount) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    T ar = a[r];
+    int64_t beg = ptr[r], end = ptr[r + 1];
+    for (int64_t base = beg; base < end; base += 32) {
+      int64_t p = base + lane;
+      bool ch = false;
+      u64 nb = 0, ob = 0;
+      if (p < end) {
+        T Q = (ag[p] == k) ? t2[p] : t1[p];
+        T pm = vmax(Q, add_rn(ar, b[idx[p]]));
+        nb = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
+        ob = res_cur[p];
+        out[p] = nb;
+        ch = nb != ob;
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, ch);
+      if (bal) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(dcount, __popc(bal));
+        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(bal & ((1u << lane) - 1));
+        if (ch && slot < kDeltaCap) { olds[slot] = ob; news[slot] = nb; }
+      }
+    }
+  }
+}
+
+// bitonic sort (ascending u64) of the first D <= kDeltaCap keys; block 0 sorts
+// olds, block 1 news, in shared memory
+__global__ void __launch_bounds__(1024) k_sort_delta(u64* __restrict__ olds, u64* __restrict__ news,
+                                                     const int* __restrict__ dcount) {
+  __shared__ u64 sh[kDeltaCap];
+  u64* a = blockIdx.x == 0 ? olds : news;
+  int D = *dcount;
+  int P = 1;
+  while (P < D) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) sh[i] = i < D ? a[i] : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int l = i ^ j;
+        if (l > i) {
+          u64 x = sh[i], y = sh[l];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) { sh[i] = y; sh[l] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < D; i += blockDim.x) a[i] = sh[i];
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const u64* __restrict__ a, int64_t n, u64 x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) { int64_t mid = (lo + hi) >> 1; if (a[mid] < x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+__device__ __forceinline__ int64_t upper_bound_u64(const u64* __restrict__ a, int64_t n, u64 x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) { int64_t mid = (lo + hi) >> 1; if (a[mid] <= x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+
+// S_new = (S_cur - olds) U news, K elements before equal news
+__global__ void k_merge_delta(int64_t N, const u64* __restrict__ S_cur, const u64* __restrict__ olds,
+                              const u64* __restrict__ news, const int* __restrict__ dcount, u64* __restrict__ out) {
+  int D = *dcount;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < N) {
+    u64 x = S_cur[t];
+    int64_t le_old = upper_bound_u64(olds, D, x);
+    int64_t lt_old = lower_bound_u64(olds, D, x);
+    bool kept = true;
+    if (le_old > lt_old) kept = (t - lower_bound_u64(S_cur, N, x)) >= le_old - lt_old;
+    if (kept) out[t - le_old + lower_bound_u64(news, D, x)] = x;
+  } else if (t < N + D) {
+    int64_t q = t - N;
+    u64 y = news[q];
+    out[q + upper_bound_u64(S_cur, N, y) - upper_bound_u64(olds, D, y)] = y;
+  }
 }
 }  // namespace stmf
