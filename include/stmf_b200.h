@@ -65,6 +65,30 @@ int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank,
                 const void* X, const uint8_t* mask, int device);
 int stmf_destroy(stmf_session* s);
 
+/*
+ * Row-sharded sessions (binary32 only).  The work rows are split
+ * into `world` contiguous blocks row_starts[s] .. row_starts[s+1]; shard s holds
+ * its block's given entries and rows of U plus a replica of V, and the fit's
+ * per-row-visit / per-batch exchanges run as NCCL collectives (MIN for the
+ * residuation minima, exact integer SUM for scores, histograms and objectives,
+ * all-gather for residuation statistics, broadcast of the visited row).  Results
+ * are bit-identical for every shard count.  One process per GPU: each calls
+ * stmf_create_sharded with its `shard` index, its block X_rows/mask_rows
+ * ((row_starts[shard+1]-row_starts[shard]) x n), the global per-row given counts
+ * row_nnz (m values) and the same NCCL unique id (from stmf_nccl_unique_id on one
+ * rank, distributed by the caller).  Factor calls then take/return the caller's
+ * rows of U and the full V.
+ */
+int stmf_nccl_unique_id(void* out, int64_t* bytes);
+int stmf_create_sharded(stmf_session** out, int dtype, int64_t m, int64_t n, int rank,
+                        const int64_t* row_starts, const int64_t* row_nnz, const void* X_rows,
+                        const uint8_t* mask_rows, int world, int shard, const void* nccl_id,
+                        int device);
+/* The same engine with `shards` row blocks inside one process on one device
+ * (collectives are kernels over the shards' buffers): the shard-invariance tests. */
+int stmf_create_sim_group(stmf_session** out, int dtype, int64_t m, int64_t n, int rank,
+                          const void* X, const uint8_t* mask, int shards, int device);
+
 /* Shape/size queries: out[0..4] = m, n, rank, given count, dtype. */
 int stmf_info(stmf_session* s, int64_t* out5);
 

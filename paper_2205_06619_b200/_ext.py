@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu"]
-HEADERS = ["stmf_kernels.cuh"]
+HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -42,6 +42,22 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+def nccl_include() -> str:
+    """nccl.h of the pip NCCL that torch loads (the library itself is dlopen'ed)."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        inc = os.path.join(base, "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    except ImportError:
+        pass
+    for c in ("/usr/include", "/usr/local/cuda/include"):
+        if os.path.exists(os.path.join(c, "nccl.h")):
+            return c
+    raise RuntimeError("nccl.h not found")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/*.cu into lib/libstmf_b200.so for sm_100a (in-tree)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
@@ -51,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB_PATH
     os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
     tmp = LIB_PATH + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *srcs]
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-I", nccl_include(), "-o", tmp, *srcs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
@@ -94,6 +110,10 @@ def lib():
         "stmf_stream": [_vp, ctypes.POINTER(_vp)],
         "stmf_set_profiling": [_vp, _int],
         "stmf_counters": [_vp, _vp],
+        "stmf_nccl_unique_id": [_vp, ctypes.POINTER(_i64)],
+        "stmf_create_sharded": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _vp, _vp, _int, _int,
+                                _vp, _int],
+        "stmf_create_sim_group": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _int, _int],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -107,7 +127,8 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_set_factors", "stmf_get_factors", "stmf_objective", "stmf_run",
                     "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
                     "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
-                    "stmf_stream", "stmf_set_profiling", "stmf_counters"]
+                    "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
+                    "stmf_create_sharded", "stmf_create_sim_group"]
 
 
 def _check(rc: int):
@@ -167,10 +188,48 @@ class Session:
         h = _vp()
         _check(lib().stmf_create(ctypes.byref(h), code, self.m, self.n, self.rank, _p(Xc), _p(Mc),
                                  default_device() if device is None else int(device)))
+        self._adopt(h)
+
+    def _adopt(self, h):
         self._h = h
         info = np.zeros(5, np.int64)
         _check(lib().stmf_info(self._h, _p(info)))
-        self.given = int(info[3])
+        self.m, self.n, self.rank, self.given = (int(x) for x in info[:4])
+        self.local_rows = self.m
+
+    @classmethod
+    def sim_group(cls, X, mask, rank: int, shards: int, device: int | None = None) -> "Session":
+        """Row-sharded engine with `shards` row blocks in this process (one device)."""
+        self = cls.__new__(cls)
+        self.dtype = np.dtype(np.float32)
+        Xc = np.ascontiguousarray(np.where(mask, X, 0), dtype=np.float32)
+        Mc = np.ascontiguousarray(mask, dtype=np.uint8)
+        h = _vp()
+        _check(lib().stmf_create_sim_group(ctypes.byref(h), STMF_F32, Xc.shape[0], Xc.shape[1], int(rank),
+                                           _p(Xc), _p(Mc), int(shards),
+                                           default_device() if device is None else int(device)))
+        self._adopt(h)
+        return self
+
+    @classmethod
+    def sharded(cls, X_rows, mask_rows, rank: int, m: int, row_starts, row_nnz, world: int, shard: int,
+                nccl_id: bytes | None, device: int | None = None) -> "Session":
+        """This process's shard of a row-sharded fit (one GPU per process, NCCL)."""
+        self = cls.__new__(cls)
+        self.dtype = np.dtype(np.float32)
+        Xc = np.ascontiguousarray(np.where(mask_rows, X_rows, 0), dtype=np.float32)
+        Mc = np.ascontiguousarray(mask_rows, dtype=np.uint8)
+        starts = np.ascontiguousarray(row_starts, dtype=np.int64)
+        nnz = np.ascontiguousarray(row_nnz, dtype=np.int64)
+        idbuf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        h = _vp()
+        _check(lib().stmf_create_sharded(ctypes.byref(h), STMF_F32, int(m), Xc.shape[1], int(rank), _p(starts),
+                                         _p(nnz), _p(Xc), _p(Mc), int(world), int(shard),
+                                         None if idbuf is None else ctypes.cast(idbuf, _vp),
+                                         default_device() if device is None else int(device)))
+        self._adopt(h)
+        self.local_rows = Xc.shape[0]
+        return self
 
     def close(self):
         if getattr(self, "_h", None):
@@ -192,8 +251,8 @@ class Session:
     # factors ---------------------------------------------------------------
     def set_factors(self, U, V=None):
         U = np.ascontiguousarray(U, dtype=self.dtype)
-        if U.shape != (self.m, self.rank):
-            raise ValueError(f"U shape {U.shape} != {(self.m, self.rank)}")
+        if U.shape != (self.local_rows, self.rank):
+            raise ValueError(f"U shape {U.shape} != {(self.local_rows, self.rank)}")
         if V is not None:
             V = np.ascontiguousarray(V, dtype=self.dtype)
             if V.shape != (self.rank, self.n):
@@ -201,7 +260,7 @@ class Session:
         _check(lib().stmf_set_factors(self._h, _p(U), None if V is None else _p(V)))
 
     def get_factors(self):
-        U = np.empty((self.m, self.rank), self.dtype)
+        U = np.empty((self.local_rows, self.rank), self.dtype)
         V = np.empty((self.rank, self.n), self.dtype)
         _check(lib().stmf_get_factors(self._h, _p(U), _p(V)))
         return U, V

@@ -901,9 +901,40 @@ struct Session : SessionBase {
   }
 };
 
+#include <memory>
+
+#include "stmf_shard.cuh"
+
 struct stmf_session {
   SessionBase* impl;
 };
+
+// contiguous row blocks with about equal given counts
+static std::vector<int64_t> balanced_row_starts(const std::vector<int64_t>& nnz, int G) {
+  int64_t m = (int64_t)nnz.size(), N = 0;
+  for (auto v : nnz) N += v;
+  std::vector<int64_t> starts(G + 1, 0);
+  starts[G] = m;
+  int64_t acc = 0, r = 0;
+  for (int s = 1; s < G; s++) {
+    int64_t target = N * s / G;
+    while (r < m - (G - s) && acc + nnz[r] <= target) acc += nnz[r++];
+    r = std::max<int64_t>(r, starts[s - 1] + 1);
+    starts[s] = r;
+  }
+  return starts;
+}
+
+static int validate_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, const void* X,
+                           const uint8_t* mask) {
+  if (!out || !X || !mask) return set_err(STMF_ERR_INVALID, "null argument");
+  if (m <= 0 || n <= 0) return set_err(STMF_ERR_INVALID, "empty matrix");
+  if (rank < 1) return set_err(STMF_ERR_INVALID, "rank must be >= 1");
+  if (rank > 255) return set_err(STMF_ERR_INVALID, "rank must be <= 255");
+  if (m >= (1ll << 31) || n >= (1ll << 31)) return set_err(STMF_ERR_INVALID, "dimension too large");
+  if (dtype != STMF_F64 && dtype != STMF_F32) return set_err(STMF_ERR_INVALID, "unknown dtype %d", dtype);
+  return STMF_OK;
+}
 
 // ----------------------------------------------------------------------------
 // C ABI
@@ -981,6 +1012,84 @@ int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, c
     return set_err(STMF_ERR_OOM, "host allocation failed");
   }
   *out = new stmf_session{impl};
+  return STMF_OK;
+}
+
+int stmf_nccl_unique_id(void* out, int64_t* bytes) {
+  if (!out || !bytes) return set_err(STMF_ERR_INVALID, "null argument");
+  if (*bytes < (int64_t)sizeof(ncclUniqueId)) {
+    *bytes = sizeof(ncclUniqueId);
+    return set_err(STMF_ERR_INVALID, "buffer too small (%d bytes needed)", (int)sizeof(ncclUniqueId));
+  }
+  GUARD({
+    ncclUniqueId id;
+    NCK(NcclApi::get().GetUniqueId(&id));
+    memcpy(out, &id, sizeof id);
+    *bytes = sizeof id;
+  });
+}
+
+int stmf_create_sharded(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, const int64_t* row_starts,
+                        const int64_t* row_nnz, const void* X_rows, const uint8_t* mask_rows, int world,
+                        int shard, const void* nccl_id, int device) {
+  int rc = validate_create(out, dtype, m, n, rank, X_rows, mask_rows);
+  if (rc) return rc;
+  if (dtype != STMF_F32) return set_err(STMF_ERR_INVALID, "sharded fits use binary32 (STMF_F32)");
+  if (!row_starts || !row_nnz || world < 1 || shard < 0 || shard >= world)
+    return set_err(STMF_ERR_INVALID, "bad shard layout");
+  if (world > 1 && !nccl_id) return set_err(STMF_ERR_INVALID, "nccl_id required for world > 1");
+  *out = nullptr;
+  ShardGroup<float>* g = nullptr;
+  try {
+    g_err.clear();
+    std::vector<int64_t> starts(row_starts, row_starts + world + 1), nnz(row_nnz, row_nnz + m);
+    if (starts[0] != 0 || starts[world] != m) fail(STMF_ERR_INVALID, "row_starts must span [0, m]");
+    for (int s = 0; s < world; s++)
+      if (starts[s + 1] <= starts[s]) fail(STMF_ERR_INVALID, "empty shard %d", s);
+    CK(cudaSetDevice(device));
+    Comm* c = world > 1 ? (Comm*)new NcclComm(world, shard, nccl_id) : (Comm*)new LocalComm(1);
+    g = new ShardGroup<float>();
+    g->dtype = dtype;
+    g->init(m, n, rank, starts, nnz, (const float*)X_rows, mask_rows, c, device);
+  } catch (const StmfError& e) {
+    delete g;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    delete g;
+    return set_err(STMF_ERR_OOM, "host allocation failed");
+  }
+  *out = new stmf_session{g};
+  return STMF_OK;
+}
+
+int stmf_create_sim_group(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, const void* X,
+                          const uint8_t* mask, int shards, int device) {
+  int rc = validate_create(out, dtype, m, n, rank, X, mask);
+  if (rc) return rc;
+  if (dtype != STMF_F32) return set_err(STMF_ERR_INVALID, "sharded fits use binary32 (STMF_F32)");
+  if (shards < 1 || shards > m) return set_err(STMF_ERR_INVALID, "bad shard count %d", shards);
+  *out = nullptr;
+  ShardGroup<float>* g = nullptr;
+  try {
+    g_err.clear();
+    std::vector<int64_t> nnz(m, 0);
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = 0; j < n; j++) nnz[i] += mask[i * n + j] != 0;
+    for (int64_t i = 0; i < m; i++)
+      if (!nnz[i]) fail(STMF_ERR_INVALID, "row %lld has no given entries", (long long)i);
+    std::vector<int64_t> starts = balanced_row_starts(nnz, shards);
+    CK(cudaSetDevice(device));
+    g = new ShardGroup<float>();
+    g->dtype = dtype;
+    g->init(m, n, rank, starts, nnz, (const float*)X, mask, new LocalComm(shards), device);
+  } catch (const StmfError& e) {
+    delete g;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    delete g;
+    return set_err(STMF_ERR_OOM, "host allocation failed");
+  }
+  *out = new stmf_session{g};
   return STMF_OK;
 }
 

@@ -315,7 +315,7 @@ __device__ __forceinline__ Top2<T> top2_warp(Top2<T> t) {
 template <typename T>
 __global__ void k_line_stats(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                              const T* __restrict__ xv, const T* __restrict__ other, T* __restrict__ s1,
-                             T* __restrict__ s2, int32_t* __restrict__ sarg) {
+                             T* __restrict__ s2, int32_t* __restrict__ sarg, int idx_offset = 0) {
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -324,7 +324,7 @@ __global__ void k_line_stats(int64_t nlines, const int64_t* __restrict__ ptr, co
     t.m1 = tinf<T>(); t.m2 = tinf<T>(); t.a1 = 0x7fffffff;
     for (int64_t p = ptr[L] + lane; p < ptr[L + 1]; p += 32) {
       int j = idx[p];
-      top2_push(t, sub_rn(xv[p], other[j]), j);
+      top2_push(t, sub_rn(xv[p], other[j]), j + idx_offset);  // argmin as a global index
     }
     t = top2_warp(t);
     if (lane == 0) { s1[L] = t.m1; s2[L] = t.m2; sarg[L] = t.a1; }
@@ -527,6 +527,7 @@ struct SideB {
   T* out;            // E x nlines: second residuation
   u64* acc;          // 2 per eval
   int* chg;          // 1 per eval
+  int mode;          // 0: min + error; 1: min only (local partial); 2: error with line values from out
 };
 
 template <int EG, typename V>
@@ -570,24 +571,31 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
   int64_t beg = S.ptr[L], end = S.ptr[L + 1];
   T mn[EG];
+  if (S.mode == 2) {
+    // sharded F-URF second half: the line values are the all-reduced minima
 #pragma unroll
-  for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-  for (int64_t p = beg + lane; p < end; p += 32) {
-    T x = S.xv[p];
-    T v[EG];
-    load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+    for (int q = 0; q < EG; q++) mn[q] = S.out[(int64_t)(e0 + (q < ne ? q : ne - 1)) * nlines + L];
+  } else {
 #pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
+    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
+    for (int64_t p = beg + lane; p < end; p += 32) {
+      T x = S.xv[p];
+      T v[EG];
+      load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+#pragma unroll
+      for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
+    }
+#pragma unroll
+    for (int q = 0; q < EG; q++)
+      for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
   }
-#pragma unroll
-  for (int q = 0; q < EG; q++)
-    for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
   if (lane < ne) {
     T w = lane_pick<EG>(mn, lane);
     int kl = lane_pick<EG>(kq, lane);
-    S.out[(int64_t)(e0 + lane) * nlines + L] = w;
-    if (w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
+    if (S.mode != 2) S.out[(int64_t)(e0 + lane) * nlines + L] = w;
+    if (S.mode != 1 && w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
   }
+  if (S.mode == 1) return;  // sharded F-URF first half: local minima only
   double part[EG];
 #pragma unroll
   for (int q = 0; q < EG; q++) part[q] = 0.0;
