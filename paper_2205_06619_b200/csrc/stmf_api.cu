@@ -248,10 +248,9 @@ struct Session : SessionBase {
   int* h_chg = nullptr;
   int* h_flags = nullptr;
   // replica
-  DevBuf<u64> res, res_sorted, res_cur, S_cur, dolds, dnews;
-  DevBuf<int> dcount;
+  DevBuf<u64> res_cur, S_cur;
   bool cur_valid = false;
-  int64_t n_delta_replicas = 0;
+  int64_t n_delta_replicas = 0, n_zero_delta = 0;
   DevBuf<double> pwval;
   DevBuf<int64_t> pw_loff;
   DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
@@ -283,7 +282,7 @@ struct Session : SessionBase {
   void counters(int64_t* out) override {
     out[0] = g_launches.load(); out[1] = g_cub_calls.load(); out[2] = phaseB_launches;
     out[3] = phaseB_ns; out[4] = phaseB_timed; out[5] = n_product_passes; out[6] = n_escalations;
-    out[7] = N;
+    out[7] = n_zero_delta;
   }
   std::vector<int> batch_sched;
 
@@ -291,6 +290,9 @@ struct Session : SessionBase {
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
     if (h_acc) cudaFreeHost(h_acc);
+    if (h_dcount) cudaFreeHost(h_dcount);
+    if (h_rep) cudaFreeHost(h_rep);
+    if (h_pwv) cudaFreeHost(h_pwv);
     if (h_chg) cudaFreeHost(h_chg);
     if (h_flags) cudaFreeHost(h_flags);
     if (st) cudaStreamDestroy(st);
@@ -346,15 +348,18 @@ struct Session : SessionBase {
       if (c == 0) fail(STMF_ERR_INVALID, "column %lld has no given entries", (long long)j);
       max_colnnz = std::max(max_colnnz, c);
     }
+    fixed_sched = !batch_sched.empty();
+    // floor of a speculative batch (candidates): the fixed per-batch cost (~40 us of
+    // launches + one host sync) ~ the cost of evaluating 8e6/N candidates
+    batch_floor = (int)std::max<int64_t>(1, std::min<int64_t>(128, 8000000 / std::max<int64_t>(N, 1)));
     if (batch_sched.empty()) {
-      // speculative batch sizes (candidates): the first batch balances the fixed
-      // per-batch cost (~40 us of launches + one host sync) against the cost of an
-      // evaluation (~N given entries); later batches grow 4x (a stuck row needs all).
+      // first visit of a row: no depth history yet
       int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
       for (int b = b0; b < Emax; b *= 4) batch_sched.push_back(b);
       batch_sched.push_back(Emax);
     }
     for (int& b : batch_sched) b = std::max(1, std::min(b, Emax));
+    row_depth.assign(m, 0);
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
@@ -384,11 +389,10 @@ struct Session : SessionBase {
     size_t b1 = 0, b2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)n, 0, 64, st));
     if (!kExact) {
-      res.alloc(N); res_sorted.alloc(N); res_cur.alloc(N); S_cur.alloc(N);
-      dolds.alloc(kDeltaCap); dnews.alloc(kDeltaCap); dcount.alloc(1);
-      CK(cub::DeviceRadixSort::SortKeys(nullptr, b2, res.p, res_sorted.p, (int64_t)N, 0, 64, st));
+      res_cur.alloc(N); S_cur.alloc(N);
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, b2, res_cur.p, S_cur.p, (int64_t)N, 0, 64, st));
       pw.build(N);
-      pwval.alloc(pw.nnodes);
+      alloc_slots();
       upload(pw_loff, pw.loff); upload(pw_llen, pw.llen); upload(pw_lnode, pw.lnode);
       upload(pw_left, pw.left); upload(pw_right, pw.right);
       upload(pw_lvloff, pw.lvl_off); upload(pw_lvlnodes, pw.lvl_nodes);
@@ -536,69 +540,157 @@ struct Session : SessionBase {
       check_flags();
       return fx_to_double(h_acc[1], h_acc[0], F);
     }
-    return replica(k, a, b);
+    return replica1(k, a, b);
   }
 
-  // numpy replica: np.sum(np.sort(|residuals|)) bit for bit (tropical.py:211)
-  double replica(int k, const T* a, const T* b) {
-    n_escalations++;
-    bool full = !cur_valid;
-    if (!full) {
-      CK(cudaMemsetAsync(dcount.p, 0, sizeof(int), st));
-      k_residuals_delta<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k,
-                                                            a, b, res_cur.p, res.p, dolds.p, dnews.p, dcount.p);
-      LAUNCH_CK();
-      CK(cudaMemcpyAsync(h_flags + 1, dcount.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      int D = h_flags[1];
-      if (D > kDeltaCap) {
-        full = true;
-      } else {
-        n_delta_replicas++;
-        if (D > 0) {
-          k_sort_delta<<<2, 1024, 0, st>>>(dolds.p, dnews.p, dcount.p);
-          LAUNCH_CK();
-        }
-        k_merge_delta<<<nblk(N + D, 256), 256, 0, st>>>(N, S_cur.p, dolds.p, dnews.p, dcount.p, res_sorted.p);
-        LAUNCH_CK();
-      }
-    } else {
-      k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, k, a, b,
-                                                      res.p);
-      LAUNCH_CK();
+  // ---- numpy replicas: np.sum(np.sort(|residuals|)) bit for bit (tropical.py:211) ----
+  // Up to kSlots candidate states are replicated per round with one host sync.  The
+  // delta path (<= kDeltaCap changed entries vs the current state) runs device-gated
+  // for every slot; slots whose change set is larger are redone with a full sort.
+  static constexpr int kSlots = 8;
+  struct Slot {
+    DevBuf<u64> res, sorted, olds, news;
+    DevBuf<int> dcount;
+    DevBuf<T> a, b;
+    DevBuf<double> pw;
+    const T* ap = nullptr;
+    const T* bp = nullptr;
+    int k = 0;
+  };
+  std::vector<Slot> slots;
+  int* h_dcount = nullptr;
+  double* h_pwv = nullptr;
+  RepSlot<T>* h_rep = nullptr;
+  DevBuf<RepSlot<T>> d_rep;
+  DevBuf<int> d_dcounts;
+
+  void alloc_slots() {
+    CK(cudaMallocHost(&h_rep, sizeof(RepSlot<T>) * kSlots));
+    d_rep.alloc(kSlots);
+    d_dcounts.alloc(kSlots);
+    slots.resize(kSlots);
+    for (auto& s : slots) {
+      s.res.alloc(N); s.sorted.alloc(N); s.olds.alloc(kDeltaCap); s.news.alloc(kDeltaCap); s.dcount.alloc(1);
+      s.a.alloc(m); s.b.alloc(n); s.pw.alloc(pw.nnodes);
     }
-    if (full) {
-      size_t bytes = cubtmp_bytes;
-      // residuals are >= 0: bit 63 is clear, sort on bits 0..62
-      CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res.p, res_sorted.p, (int64_t)N, 0, 63, st));
-      g_cub_calls++;
-    }
+    CK(cudaMallocHost(&h_dcount, sizeof(int) * kSlots));
+    CK(cudaMallocHost(&h_pwv, sizeof(double) * kSlots));
+  }
+
+  void pw_sum(Slot& s) {
     int nl = (int)pw.loff.size();
-    k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, res_sorted.p,
-                                                            pwval.p);
+    k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, s.sorted.p,
+                                                            s.pw.p);
     LAUNCH_CK();
     if (pw.H > 0) {
-      k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, pwval.p);
+      k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, s.pw.p);
       LAUNCH_CK();
     }
-    double v;
-    CK(cudaMemcpyAsync(&v, pwval.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return v;
   }
 
-  // the last replica's arrays (res, res_sorted) become the current state's
-  void adopt_replica() {
-    std::swap(res_cur.p, res.p);
-    std::swap(S_cur.p, res_sorted.p);
+  void full_sort(Slot& s) {
+    size_t bytes = cubtmp_bytes;
+    // residuals are >= 0: bit 63 is clear, sort on bits 0..62
+    CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, s.res.p, s.sorted.p, (int64_t)N, 0, 63, st));
+    g_cub_calls++;
+  }
+
+  // replicas of slots[0, count) (ap, bp, k set) -> h_pwv[s]
+  void replicas(int count) {
+    bool delta = cur_valid;
+    n_escalations += count;
+    if (delta) {
+      // one launch per step for the whole round (slot = blockIdx.y)
+      for (int i = 0; i < count; i++) {
+        Slot& s = slots[i];
+        h_rep[i] = RepSlot<T>{s.k, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p, d_dcounts.p + i, s.pw.p};
+      }
+      CK(cudaMemcpyAsync(d_rep.p, h_rep, sizeof(RepSlot<T>) * count, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(d_dcounts.p, 0, sizeof(int) * count, st));
+      dim3 g1(warps_grid(m), count);
+      k_residuals_delta_multi<T><<<g1, 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, res_cur.p,
+                                                      d_rep.p);
+      LAUNCH_CK();
+      k_sort_delta_multi<T><<<dim3(2, count), 1024, 0, st>>>(d_rep.p);
+      LAUNCH_CK();
+      k_merge_delta_multi<T><<<dim3(nblk(N + kDeltaCap, 256), count), 256, 0, st>>>(N, S_cur.p, d_rep.p);
+      LAUNCH_CK();
+      int nl = (int)pw.loff.size();
+      k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), count), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
+                                                                                     pw_lnode.p, d_rep.p);
+      LAUNCH_CK();
+      if (pw.H > 0) {
+        k_pw_combine_multi<T><<<dim3(1, count), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
+                                                                pw_right.p, d_rep.p);
+        LAUNCH_CK();
+      }
+      CK(cudaMemcpyAsync(h_dcount, d_dcounts.p, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+      for (int i = 0; i < count; i++)
+        CK(cudaMemcpyAsync(h_pwv + i, slots[i].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    for (int i = 0; i < count && !delta; i++) {
+      Slot& s = slots[i];
+      {
+        k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, s.k, s.ap,
+                                                        s.bp, s.res.p);
+        LAUNCH_CK();
+        full_sort(s);
+        h_dcount[i] = 0;
+      }
+      pw_sum(s);
+      CK(cudaMemcpyAsync(h_pwv + i, s.pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    bool redo = false;
+    for (int i = 0; i < count; i++) {
+      if (delta && h_dcount[i] == 0) n_zero_delta++;
+      if (!delta || h_dcount[i] <= kDeltaCap) {
+        n_delta_replicas += delta;
+        continue;
+      }
+      full_sort(slots[i]);
+      pw_sum(slots[i]);
+      CK(cudaMemcpyAsync(h_pwv + i, slots[i].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      redo = true;
+    }
+    if (redo) CK(cudaStreamSynchronize(st));
+  }
+
+  double replica1(int k, const T* a, const T* b) {
+    slots[0].k = k; slots[0].ap = a; slots[0].bp = b;
+    replicas(1);
+    return h_pwv[0];
+  }
+
+  // slot s's arrays become the current state's residuals / sorted residuals
+  void adopt_slot(int s) {
+    std::swap(res_cur.p, slots[s].res.p);
+    std::swap(S_cur.p, slots[s].sorted.p);
     cur_valid = true;
+  }
+
+  // point slot s at eval (op, q) of the last batch (final column k of U, row k of V)
+  void set_slot_eval(int s, int op, int q, int k) {
+    Slot& S = slots[s];
+    S.k = k;
+    if (op == 0) {
+      S.ap = ubufB.p + (size_t)q * m;
+      k_deinterleave<T><<<nblk(n, 256), 256, 0, st>>>(n, q, vbuf.p, S.b.p);
+      LAUNCH_CK();
+      S.bp = S.b.p;
+    } else {
+      k_deinterleave<T><<<nblk(m, 256), 256, 0, st>>>(m, q, ubufA.p, S.a.p);
+      LAUNCH_CK();
+      S.ap = S.a.p;
+      S.bp = vbufB.p + (size_t)q * n;
+    }
   }
 
   double objective() override {
     ensure_caches();
     if (!err_valid) {
       err = state_objective(0, Ut.p, V.p);
-      if (!kExact) adopt_replica();
+      if (!kExact) adopt_slot(0);
       err_valid = true;
     }
     return err;
@@ -629,7 +721,8 @@ struct Session : SessionBase {
   }
 
   // ---- one speculative batch: candidates cj/ck/cx[t0, t0+E) of row i ------------
-  void eval_batch(int64_t i, int64_t t0, int E) {
+  void eval_batch(int64_t i, int64_t t0, int E, int* hk = nullptr) {
+    if (hk) CK(cudaMemcpyAsync(hk, ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
     const int32_t* bj = cj.p + t0;
     const int32_t* bk = ck.p + t0;
     const T* bx = cx.p + t0;
@@ -683,34 +776,75 @@ struct Session : SessionBase {
     return dtmpB.p;
   }
 
-  // decide eval (op, q) of the current batch against err; returns 1 = accept (f set)
-  int decide(int op, int q, int E, int k, double* f) {
-    if (!h_chg[op * E + q]) return 0;  // state reproduced bit for bit: f == err
-    u64 lo = h_acc[op * 2 * E + 2 * q], hi = h_acc[op * 2 * E + 2 * q + 1];
-    double A = fx_to_double(hi, lo, F);
-    if (kExact) {
-      *f = A;
-      return A < err;
-    }
-    // fp64: |A - S| <= dr*S + da; |numpy(S) - S| <= beta*S  ("decision bound")
+  // fp64 decision bound: |A - S| <= dr*S + da, |numpy(S) - S| <= beta*S
+  double margin_of(int op, double A) const {
     int64_t L = op == 0 ? (max_rownnz + 31) / 32 : (max_colnnz + 31) / 32;
     int64_t lines = op == 0 ? m : n;
     double dr = (double)(L + 8) * std::ldexp(1.0, -53);
     double da = (double)lines * std::ldexp(1.0, -F + 1);
-    double margin = 2.0 * ((dr + beta_rel) * std::max(A, err) + da);
-    if (A - margin >= err) return 0;
-    double fr = replica(k, eval_a(op, q), eval_b(op, q));
-    if (A + margin < err && !(fr < err))
-      fail(STMF_ERR_NUMERIC, "decision bound violated: A=%.17g replica=%.17g err=%.17g", A, fr, err);
-    *f = fr;
-    return fr < err;
+    return 2.0 * ((dr + beta_rel) * std::max(A, err) + da);
   }
 
-  // accept eval (op, q); in fp64 mode its replica was the last one computed
-  void commit(int op, int q, int k) {
-    if (!kExact) adopt_replica();
-    CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, eval_a(op, q), sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(V.p + (size_t)k * n, eval_b(op, q), sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
+  // FitRun._attempt over the batch in reference order (c0 ULF, c0 URF, c1 ULF, ...):
+  // the first eval with f < err wins.  Returns the winner's order index or -1 and
+  // commits it.  fp64: evals whose bound straddles err, and the first certain
+  // accept (its numpy value becomes err), are replicated in rounds of kSlots.
+  int decide_batch(int E, const std::vector<int>& hk, double* fwin) {
+    int pos = 0;
+    while (pos < 2 * E) {
+      struct Req { int ev, q, op; bool certain; };
+      std::vector<Req> chunk;
+      int scan = pos;
+      for (; scan < 2 * E && (int)chunk.size() < (kExact ? 1 : kSlots); scan++) {
+        int q = scan >> 1, op = scan & 1;
+        if (!h_chg[op * E + q]) continue;  // state reproduced bit for bit: f == err
+        double A = fx_to_double(h_acc[op * 2 * E + 2 * q + 1], h_acc[op * 2 * E + 2 * q], F);
+        if (kExact) {
+          if (A < err) {
+            commit_eval(op, q, hk[q], -1);
+            *fwin = A;
+            return scan;
+          }
+          continue;
+        }
+        double mg = margin_of(op, A);
+        if (A - mg >= err) continue;  // certainly not below err
+        chunk.push_back({scan, q, op, A + mg < err});
+        if (A + mg < err) { scan++; break; }
+      }
+      if (!chunk.empty()) {
+        for (size_t c = 0; c < chunk.size(); c++) set_slot_eval((int)c, chunk[c].op, chunk[c].q, hk[chunk[c].q]);
+        replicas((int)chunk.size());
+        for (size_t c = 0; c < chunk.size(); c++) {
+          double fr = h_pwv[c];
+          if (fr < err) {
+            commit_eval(chunk[c].op, chunk[c].q, hk[chunk[c].q], (int)c);
+            *fwin = fr;
+            return chunk[c].ev;
+          }
+          if (chunk[c].certain)
+            fail(STMF_ERR_NUMERIC, "decision bound violated: replica=%.17g err=%.17g", fr, err);
+        }
+      }
+      pos = scan;
+    }
+    return -1;
+  }
+
+  // accept eval (op, q); fp64: `slot` holds its replica (residuals of the new state)
+  void commit_eval(int op, int q, int k, int slot) {
+    const T* a;
+    const T* b;
+    if (slot >= 0) {
+      adopt_slot(slot);
+      a = slots[slot].ap;
+      b = slots[slot].bp;
+    } else {
+      a = eval_a(op, q);
+      b = eval_b(op, q);
+    }
+    CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, a, sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(V.p + (size_t)k * n, b, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
     dirty = true;
     stats_dirty[k] = 1;
   }
@@ -732,38 +866,69 @@ struct Session : SessionBase {
   }
 
   // byrow_sweep(run, i, "TD_A") (strategies.py:191-224)
+  // STMF_PHASE_TIMING=1: synchronise after every phase and accumulate wall time
+  // (diagnostics only; perturbs the overlap it measures)
+  bool phase_timing = getenv("STMF_PHASE_TIMING") != nullptr;
+  double ph[6] = {0, 0, 0, 0, 0, 0};  // caches, candidates, batch eval, decide+replicas, commit, other
+  double ph_t = 0;
+  void ph_mark(int slot) {
+    if (!phase_timing) return;
+    CK(cudaStreamSynchronize(st));
+    double t = now_s();
+    if (slot >= 0) ph[slot] += t - ph_t;
+    ph_t = t;
+  }
+  void ph_report() {
+    if (phase_timing)
+      fprintf(stderr, "[stmf phases ms] caches %.1f candidates %.1f eval %.1f decide %.1f\n", ph[0] * 1e3,
+              ph[1] * 1e3, ph[2] * 1e3, ph[3] * 1e3);
+  }
+
   void row_visit(RunState& R, int64_t i) {
+    ph_mark(-1);
     ensure_caches();
+    ph_mark(0);
     int64_t nc = build_candidates(i);
+    ph_mark(1);
     R.visits++;
     std::vector<int> hk;
     int64_t t0 = 0;
     size_t bi = 0;
+    // speculation depth: a row's acceptance depth is strongly correlated across
+    // sweeps, so the first batch covers 1.25x the candidates the row consumed on
+    // its previous visit, floored by the fixed per-batch cost; then 2x growth
+    int first = batch_sched[0];
+    if (!fixed_sched && (int64_t)row_depth.size() == m && row_depth[i] > 0)
+      first = (int)std::max<int64_t>(batch_floor, std::min<int64_t>(Emax, row_depth[i] + row_depth[i] / 4 + 2));
+    int next = first;
     while (t0 < nc) {
-      int E = (int)std::min<int64_t>(nc - t0, batch_sched[std::min(bi, batch_sched.size() - 1)]);
+      int E = (int)std::min<int64_t>(nc - t0, fixed_sched ? batch_sched[std::min(bi, batch_sched.size() - 1)] : next);
       bi++;
-      eval_batch(i, t0, E);
+      next = std::min(Emax, 2 * next);
       hk.resize(E);
-      CK(cudaMemcpyAsync(hk.data(), ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      eval_batch(i, t0, E, hk.data());  // one host sync per batch
+      ph_mark(2);
       R.evaluated += 2 * (int64_t)E;
-      for (int q = 0; q < E; q++) {
-        for (int op = 0; op < 2; op++) {
-          R.attempts++;
-          double f;
-          if (decide(op, q, E, hk[q], &f)) {
-            commit(op, q, hk[q]);
-            err = f;
-            R.accepts++;
-            traj_append(R, run_now(R), err);
-            return;
-          }
-        }
+      double f;
+      int w = decide_batch(E, hk, &f);
+      ph_mark(3);
+      if (w >= 0) {
+        R.attempts += w + 1;
+        if ((int64_t)row_depth.size() == m) row_depth[i] = t0 + w / 2 + 1;
+        err = f;
+        R.accepts++;
+        traj_append(R, run_now(R), err);
+        return;
       }
+      R.attempts += 2 * (int64_t)E;
       if (out_of_time(R)) return;
       t0 += E;
     }
+    if ((int64_t)row_depth.size() == m) row_depth[i] = nc;
   }
+  std::vector<int64_t> row_depth;  // candidates consumed at each row's last visit
+  int batch_floor = 1;
+  bool fixed_sched = false;
 
   void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
            int64_t* counts) override {
@@ -795,6 +960,7 @@ struct Session : SessionBase {
       }
     }
     counts[0] = R.len; counts[1] = R.attempts; counts[2] = R.accepts; counts[3] = sweeps;
+    ph_report();
     counts[4] = R.visits; counts[5] = R.evaluated; counts[6] = n_escalations - esc0;
     counts[7] = n_product_passes - pp0;
   }
@@ -857,7 +1023,9 @@ struct Session : SessionBase {
     } else if (kExact) {
       fv = fx_to_double(h_acc[op * 2 + 1], h_acc[op * 2], F);
     } else {
-      fv = replica(k, eval_a(op, 0), eval_b(op, 0));
+      set_slot_eval(0, op, 0, k);
+      replicas(1);
+      fv = h_pwv[0];
     }
     if (ucol) CK(cudaMemcpyAsync(ucol, eval_a(op, 0), sizeof(T) * m, cudaMemcpyDeviceToHost, st));
     if (vrow) CK(cudaMemcpyAsync(vrow, eval_b(op, 0), sizeof(T) * n, cudaMemcpyDeviceToHost, st));
@@ -865,7 +1033,10 @@ struct Session : SessionBase {
     *f = fv;
     if (commit_if_better) {
       *accepted = fv < err;
-      if (*accepted) { commit(op, 0, k); err = fv; }
+      if (*accepted) {
+        commit_eval(op, 0, k, kExact ? -1 : 0);
+        err = fv;
+      }
     }
   }
 

@@ -886,6 +886,7 @@ __global__ void __launch_bounds__(1024) k_sort_delta(u64* __restrict__ olds, u64
   __shared__ u64 sh[kDeltaCap];
   u64* a = blockIdx.x == 0 ? olds : news;
   int D = *dcount;
+  if (D > kDeltaCap) return;  // full-sort fallback on the host side
   int P = 1;
   while (P < D) P <<= 1;
   for (int i = threadIdx.x; i < P; i += blockDim.x) sh[i] = i < D ? a[i] : ~0ull;
@@ -921,6 +922,7 @@ __device__ __forceinline__ int64_t upper_bound_u64(const u64* __restrict__ a, in
 __global__ void k_merge_delta(int64_t N, const u64* __restrict__ S_cur, const u64* __restrict__ olds,
                               const u64* __restrict__ news, const int* __restrict__ dcount, u64* __restrict__ out) {
   int D = *dcount;
+  if (D > kDeltaCap) return;  // full-sort fallback on the host side
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < N) {
     u64 x = S_cur[t];
@@ -933,6 +935,154 @@ __global__ void k_merge_delta(int64_t N, const u64* __restrict__ S_cur, const u6
     int64_t q = t - N;
     u64 y = news[q];
     out[q + upper_bound_u64(S_cur, N, y) - upper_bound_u64(olds, D, y)] = y;
+  }
+}
+
+// ---- the same replica steps for a round of slots in one launch each (slot = blockIdx.y)
+template <typename T>
+struct RepSlot {
+  int k;
+  const T* a;
+  const T* b;
+  u64* res;
+  u64* sorted;
+  u64* olds;
+  u64* news;
+  int* dcount;
+  double* pw;
+};
+
+template <typename T>
+__global__ void k_residuals_delta_multi(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                        const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
+                                        const uint8_t* __restrict__ ag, const u64* __restrict__ res_cur,
+                                        const RepSlot<T>* __restrict__ slots) {
+  const RepSlot<T> S = slots[blockIdx.y];
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    T ar = S.a[r];
+    int64_t beg = ptr[r], end = ptr[r + 1];
+    for (int64_t base = beg; base < end; base += 32) {
+      int64_t p = base + lane;
+      bool ch = false;
+      u64 nb = 0, ob = 0;
+      if (p < end) {
+        T Q = (ag[p] == S.k) ? t2[p] : t1[p];
+        T pm = vmax(Q, add_rn(ar, S.b[idx[p]]));
+        nb = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
+        ob = res_cur[p];
+        S.res[p] = nb;
+        ch = nb != ob;
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, ch);
+      if (bal) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(S.dcount, __popc(bal));
+        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(bal & ((1u << lane) - 1));
+        if (ch && slot < kDeltaCap) { S.olds[slot] = ob; S.news[slot] = nb; }
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_sort_delta_multi(const RepSlot<T>* __restrict__ slots) {
+  const RepSlot<T> S = slots[blockIdx.y];
+  __shared__ u64 sh[kDeltaCap];
+  u64* a = blockIdx.x == 0 ? S.olds : S.news;
+  int D = *S.dcount;
+  if (D > kDeltaCap || D < 2) return;
+  int P = 1;
+  while (P < D) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) sh[i] = i < D ? a[i] : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int l = i ^ j;
+        if (l > i) {
+          u64 x = sh[i], y = sh[l];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) { sh[i] = y; sh[l] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < D; i += blockDim.x) a[i] = sh[i];
+}
+
+template <typename T>
+__global__ void k_merge_delta_multi(int64_t N, const u64* __restrict__ S_cur, const RepSlot<T>* __restrict__ slots) {
+  const RepSlot<T> S = slots[blockIdx.y];
+  int D = *S.dcount;
+  if (D > kDeltaCap) return;
+  const u64* __restrict__ olds = S.olds;
+  const u64* __restrict__ news = S.news;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < N) {
+    u64 x = S_cur[t];
+    int64_t le_old = upper_bound_u64(olds, D, x);
+    int64_t lt_old = lower_bound_u64(olds, D, x);
+    bool kept = true;
+    if (le_old > lt_old) kept = (t - lower_bound_u64(S_cur, N, x)) >= le_old - lt_old;
+    if (kept) S.sorted[t - le_old + lower_bound_u64(news, D, x)] = x;
+  } else if (t < N + D) {
+    int64_t q = t - N;
+    u64 y = news[q];
+    S.sorted[q + upper_bound_u64(S_cur, N, y) - upper_bound_u64(olds, D, y)] = y;
+  }
+}
+
+template <typename T>
+__global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff, const int32_t* __restrict__ llen,
+                                   const int32_t* __restrict__ lnode, const RepSlot<T>* __restrict__ slots) {
+  const RepSlot<T> S = slots[blockIdx.y];
+  int lane = threadIdx.x & 31;
+  int j = lane & 7;
+  int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3);
+  bool ok = t < nleaves;
+  const double* a = reinterpret_cast<const double*>(S.sorted) + (ok ? loff[t] : 0);
+  int n = ok ? llen[t] : 0;
+  double r = 0.0;
+  int body = n - (n % 8);
+  if (n >= 8) {
+    r = a[j];
+    for (int i = 8 + j; i < body; i += 8) r = __dadd_rn(r, a[i]);
+  }
+  double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+  double r2 = __shfl_down_sync(0xffffffffu, r, 2);
+  double r3 = __shfl_down_sync(0xffffffffu, r, 3);
+  double r4 = __shfl_down_sync(0xffffffffu, r, 4);
+  double r5 = __shfl_down_sync(0xffffffffu, r, 5);
+  double r6 = __shfl_down_sync(0xffffffffu, r, 6);
+  double r7 = __shfl_down_sync(0xffffffffu, r, 7);
+  if (ok && j == 0) {
+    double res;
+    if (n < 8) {
+      res = 0.0;
+      for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    } else {
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r, r1), __dadd_rn(r2, r3)), __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+      for (int i = body; i < n; i++) res = __dadd_rn(res, a[i]);
+    }
+    S.pw[lnode[t]] = res;
+  }
+}
+
+template <typename T>
+__global__ void k_pw_combine_multi(int H, const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ nodes,
+                                   const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                                   const RepSlot<T>* __restrict__ slots) {
+  double* val = slots[blockIdx.y].pw;
+  for (int h = 0; h < H; h++) {
+    for (int t = lvl_off[h] + threadIdx.x; t < lvl_off[h + 1]; t += blockDim.x) {
+      int nd = nodes[t];
+      val[nd] = __dadd_rn(val[left[nd]], val[right[nd]]);
+    }
+    __syncthreads();
   }
 }
 }  // namespace stmf

@@ -13,7 +13,10 @@ t = time.time()
 s = _ext.Session(work.values, work.mask, C["rank"]); s.set_factors(U0)
 print("session", time.time() - t, "given", s.given, flush=True)
 for sw in range(sweeps):
+    c0 = s.counters()
     t = time.time()
     tt, te, cnt = s.run(budget_sweeps=1, epsilon=0.0)
     dt = time.time() - t
-    print(f"sweep {sw+1}: {dt*1e3:.1f} ms err {te[0]:.6f}->{te[-1]:.6f} {cnt}", flush=True)
+    c1 = s.counters()
+    d = {k: c1[k] - c0[k] for k in c1}
+    print(f"sweep {sw+1}: {dt*1e3:.1f} ms err {te[0]:.6f}->{te[-1]:.6f} {cnt} delta {d}", flush=True)
