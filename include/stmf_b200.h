@@ -156,6 +156,20 @@ int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, c
  */
 int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, double* err);
 
+/*
+ * Config-5 kernel microbench (BASELINE.json configs[4]): masked max-plus product +
+ * error reduction over an m x n binary32 matrix generated on the device (seeded:
+ * X, U, V ~ U[-1,1) on the 2^-23 grid, iid given-mask of the given density,
+ * bit-packed).  m % 64 == 0, n % 128 == 0.  Runs `reps` timed launches (CUDA
+ * events; L2 flushed between reps when flush_l2).  out6 = {avg ms, best ms,
+ * objective (exact sum), given count, algorithmic GB/s (X + mask + factors),
+ * dense G (entry, k)/s}.  X_out (m*n), mask_out (m*n/32 words), U_out (rank x m,
+ * k-major) and V_out (rank x n) receive the generated data when non-NULL.
+ */
+int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps,
+                       int flush_l2, int device, double* out6, float* X_out, uint32_t* mask_out,
+                       float* U_out, float* V_out);
+
 /* ---- measurement plumbing ---- */
 
 /* The session's cudaStream_t (all device work of the session is ordered on it). */

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu"]
-HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh"]
+HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -114,6 +114,8 @@ def lib():
         "stmf_create_sharded": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _vp, _vp, _int, _int,
                                 _vp, _int],
         "stmf_create_sim_group": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _int, _int],
+        "stmf_bench_maxplus": [_i64, _i64, _int, _dbl, ctypes.c_uint64, _int, _int, _int, _vp, _vp, _vp, _vp,
+                               _vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -128,7 +130,26 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
                     "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
                     "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
-                    "stmf_create_sharded", "stmf_create_sim_group"]
+                    "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus"]
+
+
+def bench_maxplus(m: int, n: int, rank: int, density: float, seed: int = 0, reps: int = 5,
+                  flush_l2: bool = True, device: int | None = None, want_data: bool = False):
+    """Config-5 masked max-plus product + error microbench on device-generated data."""
+    out = np.zeros(6, np.float64)
+    X = np.empty((m, n), np.float32) if want_data else None
+    M = np.empty(m * n // 32, np.uint32) if want_data else None
+    U = np.empty((rank, m), np.float32) if want_data else None
+    V = np.empty((rank, n), np.float32) if want_data else None
+    p = lambda a: None if a is None else _p(a)  # noqa: E731
+    _check(lib().stmf_bench_maxplus(m, n, rank, float(density), int(seed), int(reps), int(flush_l2),
+                                    default_device() if device is None else int(device), _p(out),
+                                    p(X), p(M), p(U), p(V)))
+    res = dict(zip(("avg_ms", "best_ms", "objective", "given", "gbs", "gpairs_per_s"), out.tolist()))
+    if want_data:
+        mask = np.unpackbits(M.view(np.uint8), bitorder="little").reshape(m, n).astype(bool)
+        res["data"] = (X, mask, U.T.copy(), V)
+    return res
 
 
 def _check(rc: int):

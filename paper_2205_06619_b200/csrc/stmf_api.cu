@@ -251,6 +251,7 @@ struct Session : SessionBase {
   DevBuf<u64> res_cur, S_cur;
   bool cur_valid = false;
   int64_t n_delta_replicas = 0, n_zero_delta = 0;
+  int unroll = 1;  // phase-B entries per lane per iteration (STMF_UNROLL)
   DevBuf<double> pwval;
   DevBuf<int64_t> pw_loff;
   DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
@@ -311,6 +312,7 @@ struct Session : SessionBase {
     CK(cudaGetDeviceProperties(&prop, dev));
     nsm = prop.multiProcessorCount;
     if (const char* e = getenv("STMF_EMAX")) Emax = std::max(8, atoi(e));
+    if (const char* e = getenv("STMF_UNROLL")) unroll = atoi(e);
     Emax = (Emax + kEG - 1) / kEG * kEG;
     batch_sched.clear();  // filled once N is known (see below)
     if (const char* e = getenv("STMF_BATCH")) {
@@ -747,7 +749,7 @@ struct Session : SessionBase {
     SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf};
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
-    k_phaseB<T><<<warps_grid((m + n) * ng), 256, 0, st>>>(sa, sb, E, bk, flags.p, F, exact_limit);
+    launch_phaseB<T>(unroll, warps_grid((m + n) * ng), st, sa, sb, E, bk, flags.p, F, exact_limit);
     LAUNCH_CK();
     if (profiling) CK(cudaEventRecord(ev_b1, st));
     phaseB_launches++;
@@ -1074,7 +1076,95 @@ struct Session : SessionBase {
 
 #include <memory>
 
+#include "stmf_maxplus.cuh"
 #include "stmf_shard.cuh"
+
+__global__ void k_popcount(int64_t words, const uint32_t* __restrict__ mask, u64* __restrict__ out) {
+  u64 c = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(mask[w]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+// config-5 microbench: data generated on the device (seeded counter-based RNG:
+// X, U, V ~ U[-1, 1) on the 2^-23 grid, iid mask with P(given) = density)
+static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint64_t seed, int reps, int flush,
+                               int device, double* out, float* X_out, uint32_t* mask_out, float* U_out,
+                               float* V_out) {
+  if (m % kMpTR || n % kMpTC) fail(STMF_ERR_INVALID, "m must be a multiple of %d and n of %d", kMpTR, kMpTC);
+  if (r < 1) fail(STMF_ERR_INVALID, "rank must be >= 1");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevBuf<float> X, Ut, V;
+  DevBuf<uint32_t> M;
+  DevBuf<u64> acc, cnt;
+  DevBuf<int> flags;
+  DevBuf<uint8_t> scratch;
+  int64_t words = m * n / 32;
+  X.alloc((size_t)(m * n)); M.alloc((size_t)words); Ut.alloc((size_t)r * m); V.alloc((size_t)r * n);
+  acc.alloc(2); cnt.alloc(1); flags.alloc(1);
+  unsigned gb = (unsigned)prop.multiProcessorCount * 8;
+  k_gen_uniform<<<gb, 256, 0, st>>>(m * n, seed * 4 + 0, X.p); LAUNCH_CK();
+  k_gen_uniform<<<gb, 256, 0, st>>>((int64_t)r * m, seed * 4 + 1, Ut.p); LAUNCH_CK();
+  k_gen_uniform<<<gb, 256, 0, st>>>((int64_t)r * n, seed * 4 + 2, V.p); LAUNCH_CK();
+  uint32_t thr = (uint32_t)std::min(16777216.0, std::max(0.0, density * 16777216.0));
+  k_gen_mask<<<gb, 256, 0, st>>>(words, seed * 4 + 3, thr, M.p); LAUNCH_CK();
+  CK(cudaMemsetAsync(cnt.p, 0, sizeof(u64), st));
+  k_popcount<<<gb, 256, 0, st>>>(words, M.p, cnt.p); LAUNCH_CK();
+  if (flush) scratch.alloc((size_t)256 << 20);
+  int F = 23;  // every value is a multiple of 2^-23
+  double exact_limit = std::ldexp(1.0, 53 - F);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  dim3 grid((unsigned)(n / kMpTC), (unsigned)(m / kMpTR));
+  CK(cudaFuncSetAttribute(k_maxplus_err<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+  CK(cudaFuncSetAttribute(k_maxplus_err<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+  CK(cudaFuncSetAttribute(k_maxplus_err<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+  auto kern = r <= 4 ? k_maxplus_err<4> : r <= 8 ? k_maxplus_err<8> : k_maxplus_err<16>;
+  double total = 0, best = 1e30;
+  u64 h[2] = {0, 0};
+  for (int rep = 0; rep < std::max(reps, 1); rep++) {
+    if (flush) CK(cudaMemsetAsync(scratch.p, rep & 0xff, scratch.n, st));
+    CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
+    CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+    CK(cudaEventRecord(e0, st));
+    kern<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit);
+    LAUNCH_CK();
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    total += ms;
+    best = std::min(best, (double)ms);
+  }
+  int hf = 0;
+  u64 given = 0;
+  CK(cudaMemcpyAsync(h, acc.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hf, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&given, cnt.p, sizeof(u64), cudaMemcpyDeviceToHost, st));
+  if (X_out) CK(cudaMemcpyAsync(X_out, X.p, sizeof(float) * m * n, cudaMemcpyDeviceToHost, st));
+  if (mask_out) CK(cudaMemcpyAsync(mask_out, M.p, sizeof(uint32_t) * words, cudaMemcpyDeviceToHost, st));
+  if (U_out) CK(cudaMemcpyAsync(U_out, Ut.p, sizeof(float) * r * m, cudaMemcpyDeviceToHost, st));
+  if (V_out) CK(cudaMemcpyAsync(V_out, V.p, sizeof(float) * r * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  if (hf & 6) fail(STMF_ERR_NUMERIC, "exact objective window violated (flags %d)", hf);
+  double avg = total / std::max(reps, 1);
+  double bytes = (double)m * n * 4.0 + (double)words * 4.0 + (double)r * (m + n) * 4.0;
+  out[0] = avg;
+  out[1] = best;
+  out[2] = fx_to_double(h[1], h[0], F);
+  out[3] = (double)given;
+  out[4] = bytes / (avg * 1e-3) / 1e9;                    // algorithmic GB/s
+  out[5] = (double)m * n * r / (avg * 1e-3) / 1e9;        // G (entry, k) pairs / s (dense)
+}
 
 struct stmf_session {
   SessionBase* impl;
@@ -1184,6 +1274,12 @@ int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, c
   }
   *out = new stmf_session{impl};
   return STMF_OK;
+}
+
+int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps, int flush_l2,
+                       int device, double* out6, float* X_out, uint32_t* mask_out, float* U_out, float* V_out) {
+  if (!out6) return set_err(STMF_ERR_INVALID, "null output");
+  GUARD(maxplus_bench_impl(m, n, rank, density, seed, reps, flush_l2, device, out6, X_out, mask_out, U_out, V_out));
 }
 
 int stmf_nccl_unique_id(void* out, int64_t* bytes) {

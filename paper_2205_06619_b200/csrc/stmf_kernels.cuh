@@ -553,7 +553,7 @@ __device__ __forceinline__ void load_eg(const double* __restrict__ g, int64_t le
   }
 }
 
-template <typename T>
+template <typename T, int UNR>
 __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E, const int32_t* __restrict__ ek,
                                             int lane, int* __restrict__ flags, int F, double exact_limit) {
   constexpr int EG = kEG;
@@ -578,12 +578,26 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   } else {
 #pragma unroll
     for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-    for (int64_t p = beg + lane; p < end; p += 32) {
-      T x = S.xv[p];
-      T v[EG];
-      load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+    // U entries per lane per iteration: their idx -> vin gathers are in flight
+    // together (the loop is latency-bound otherwise); missing slots use x = +inf
+    constexpr int U = UNR;
+    for (int64_t p0 = beg + lane; p0 < end; p0 += 32 * U) {
+      T x[U];
+      int c[U];
 #pragma unroll
-      for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
+      for (int u = 0; u < U; u++) {
+        int64_t p = p0 + 32 * u;
+        bool ok = p < end;
+        x[u] = ok ? S.xv[p] : tinf<T>();
+        c[u] = ok ? S.idx[p] : 0;
+      }
+      T v[U][EG];
+#pragma unroll
+      for (int u = 0; u < U; u++) load_eg(vg, S.len_other, (int64_t)c[u], v[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x[u], v[u][q]));
     }
 #pragma unroll
     for (int q = 0; q < EG; q++)
@@ -599,17 +613,33 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   double part[EG];
 #pragma unroll
   for (int q = 0; q < EG; q++) part[q] = 0.0;
-  for (int64_t p = beg + lane; p < end; p += 32) {
-    T x = S.xv[p];
-    T a1 = S.t1[p], a2 = S.t2[p];
-    int a = S.ag[p];
-    T v[EG];
-    load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+  constexpr int U2 = UNR;
+  for (int64_t p0 = beg + lane; p0 < end; p0 += 32 * U2) {
+    T x[U2], a1[U2], a2[U2];
+    int a[U2], c[U2];
 #pragma unroll
-    for (int q = 0; q < EG; q++) {
-      T Q = (a == kq[q]) ? a2 : a1;
-      T pm = vmax(Q, add_rn(mn[q], v[q]));
-      part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
+    for (int u = 0; u < U2; u++) {
+      int64_t p = p0 + 32 * u;
+      bool ok = p < end;
+      int64_t pp = ok ? p : beg;
+      x[u] = S.xv[pp];
+      c[u] = S.idx[pp];
+      a1[u] = S.t1[pp];
+      a2[u] = S.t2[pp];
+      a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the line (contributes 0)
+    }
+    T v[U2][EG];
+#pragma unroll
+    for (int u = 0; u < U2; u++) load_eg(vg, S.len_other, (int64_t)c[u], v[u]);
+#pragma unroll
+    for (int u = 0; u < U2; u++) {
+      if (a[u] < 0) continue;
+#pragma unroll
+      for (int q = 0; q < EG; q++) {
+        T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
+        T pm = vmax(Q, add_rn(mn[q], v[u][q]));
+        part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
+      }
     }
   }
 #pragma unroll
@@ -628,8 +658,9 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
 
 // Phase B of both update rules in one launch: items [0, A) are F-ULF evals on CSR
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
-template <typename T>
-__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 4)
+// UNR = entries per lane per loop iteration (memory-level parallelism vs registers)
+template <typename T, int UNR>
+__global__ void __launch_bounds__(256, (sizeof(T) == 8 || UNR > 1) ? 2 : 3)
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
          double exact_limit) {
   int lane = threadIdx.x & 31;
@@ -638,9 +669,17 @@ k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __r
   int ngroups = (E + kEG - 1) / kEG;
   int64_t itemsA = A.nlines * ngroups, items = itemsA + B.nlines * ngroups;
   for (int64_t it = w; it < items; it += nw) {
-    if (it < itemsA) phaseB_item<T>(A, it, E, ek, lane, flags, F, exact_limit);
-    else phaseB_item<T>(B, it - itemsA, E, ek, lane, flags, F, exact_limit);
+    if (it < itemsA) phaseB_item<T, UNR>(A, it, E, ek, lane, flags, F, exact_limit);
+    else phaseB_item<T, UNR>(B, it - itemsA, E, ek, lane, flags, F, exact_limit);
   }
+}
+
+template <typename T>
+inline void launch_phaseB(int unroll, unsigned grid, cudaStream_t st, const SideB<T>& A, const SideB<T>& B, int E,
+                          const int32_t* ek, int* flags, int F, double exact_limit) {
+  if (unroll >= 4) k_phaseB<T, 4><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
+  else if (unroll == 2) k_phaseB<T, 2><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
+  else k_phaseB<T, 1><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
 }
 
 // Exact/bounded objective of an explicit state: entries' residual |x - max(Q^k, a_r + b_c)|

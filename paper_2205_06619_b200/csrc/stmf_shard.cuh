@@ -320,6 +320,7 @@ struct ShardGroup : SessionBase {
   int* h_chg = nullptr;
   int* h_flags = nullptr;
   int64_t n_product_passes = 0;
+  int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 1;
   size_t off_x = 0, off_h = 0, off_u = 0, rowbuf_bytes = 0;
   int gridX = -1000;
 
@@ -686,7 +687,7 @@ struct ShardGroup : SessionBase {
                   s.acc.p, s.chg.p, 0};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
                   s.acc.p + 2 * (size_t)E, s.chg.p + E, 1};
-      k_phaseB<T><<<warps_grid((s.ml + n) * ng), 256, 0, st>>>(sa, sb, E, bk, s.flags.p, F, exact_limit);
+      launch_phaseB<T>(unroll, warps_grid((s.ml + n) * ng), st, sa, sb, E, bk, s.flags.p, F, exact_limit);
       LAUNCH_CK();
     }
     // F-URF: v''_c = min over ALL rows -> all-reduce MIN of the local column minima
@@ -699,7 +700,7 @@ struct ShardGroup : SessionBase {
                     s.acc.p, s.chg.p, 0};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
                   s.acc.p + 2 * (size_t)E, s.chg.p + E, 2};
-      k_phaseB<T><<<warps_grid(n * ng), 256, 0, st>>>(none, sb, E, bk, s.flags.p, F, exact_limit);
+      launch_phaseB<T>(unroll, warps_grid(n * ng), st, none, sb, E, bk, s.flags.p, F, exact_limit);
       LAUNCH_CK();
     }
     reduce_acc(2 * E);
