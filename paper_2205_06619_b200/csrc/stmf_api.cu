@@ -251,7 +251,7 @@ struct Session : SessionBase {
   DevBuf<u64> res_cur, S_cur;
   bool cur_valid = false;
   int64_t n_delta_replicas = 0, n_zero_delta = 0;
-  int unroll = 1;  // phase-B entries per lane per iteration (STMF_UNROLL)
+  int unroll = sizeof(T) == 4 ? 2 : 1;  // phase-B pass-2 entries per lane per iteration (STMF_UNROLL)
   DevBuf<double> pwval;
   DevBuf<int64_t> pw_loff;
   DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
@@ -313,6 +313,7 @@ struct Session : SessionBase {
     nsm = prop.multiProcessorCount;
     if (const char* e = getenv("STMF_EMAX")) Emax = std::max(8, atoi(e));
     if (const char* e = getenv("STMF_UNROLL")) unroll = atoi(e);
+    read_sched_env();
     Emax = (Emax + kEG - 1) / kEG * kEG;
     batch_sched.clear();  // filled once N is known (see below)
     if (const char* e = getenv("STMF_BATCH")) {
@@ -362,6 +363,11 @@ struct Session : SessionBase {
     }
     for (int& b : batch_sched) b = std::max(1, std::min(b, Emax));
     row_depth.assign(m, 0);
+    // measured (profiles/r01_sched.md): launch-bound small problems prefer generous
+    // batches, evaluation-bound large ones tight batches with slow growth
+    if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = 1.5; }
+    read_sched_env();
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
@@ -901,12 +907,13 @@ struct Session : SessionBase {
     // its previous visit, floored by the fixed per-batch cost; then 2x growth
     int first = batch_sched[0];
     if (!fixed_sched && (int64_t)row_depth.size() == m && row_depth[i] > 0)
-      first = (int)std::max<int64_t>(batch_floor, std::min<int64_t>(Emax, row_depth[i] + row_depth[i] / 4 + 2));
+      first = (int)std::max<int64_t>(batch_floor,
+                                     std::min<int64_t>(Emax, (int64_t)(sched_scale * row_depth[i]) + sched_add));
     int next = first;
     while (t0 < nc) {
       int E = (int)std::min<int64_t>(nc - t0, fixed_sched ? batch_sched[std::min(bi, batch_sched.size() - 1)] : next);
       bi++;
-      next = std::min(Emax, 2 * next);
+      next = std::min(Emax, std::max(next + 1, (int)(next * sched_growth)));
       hk.resize(E);
       eval_batch(i, t0, E, hk.data());  // one host sync per batch
       ph_mark(2);
@@ -916,7 +923,10 @@ struct Session : SessionBase {
       ph_mark(3);
       if (w >= 0) {
         R.attempts += w + 1;
-        if ((int64_t)row_depth.size() == m) row_depth[i] = t0 + w / 2 + 1;
+        if ((int64_t)row_depth.size() == m) {
+          row_depth[i] = t0 + w / 2 + 1;
+          depth_ema = depth_ema > 0 ? 0.9 * depth_ema + 0.1 * (double)row_depth[i] : (double)row_depth[i];
+        }
         err = f;
         R.accepts++;
         traj_append(R, run_now(R), err);
@@ -929,6 +939,13 @@ struct Session : SessionBase {
     if ((int64_t)row_depth.size() == m) row_depth[i] = nc;
   }
   std::vector<int64_t> row_depth;  // candidates consumed at each row's last visit
+  double depth_ema = 0;            // running mean of accepting depths
+  // first batch = scale * previous depth + add; later batches grow by `growth`
+  double sched_scale = 1.25, sched_growth = 2.0;
+  int sched_add = 2;
+  void read_sched_env() {
+    if (const char* e = getenv("STMF_SCHED")) sscanf(e, "%lf,%d,%lf", &sched_scale, &sched_add, &sched_growth);
+  }
   int batch_floor = 1;
   bool fixed_sched = false;
 

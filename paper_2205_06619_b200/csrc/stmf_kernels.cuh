@@ -580,7 +580,7 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
     for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
     // U entries per lane per iteration: their idx -> vin gathers are in flight
     // together (the loop is latency-bound otherwise); missing slots use x = +inf
-    constexpr int U = UNR;
+    constexpr int U = sizeof(T) == 8 ? 2 : 4;  // pass 1 is cheap in registers: always unrolled
     for (int64_t p0 = beg + lane; p0 < end; p0 += 32 * U) {
       T x[U];
       int c[U];
@@ -660,7 +660,7 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
 // UNR = entries per lane per loop iteration (memory-level parallelism vs registers)
 template <typename T, int UNR>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 || UNR > 1) ? 2 : 3)
+__global__ void __launch_bounds__(256, (sizeof(T) == 8 || UNR > 2) ? 2 : 3)
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
          double exact_limit) {
   int lane = threadIdx.x & 31;

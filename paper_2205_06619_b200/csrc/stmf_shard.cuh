@@ -320,7 +320,7 @@ struct ShardGroup : SessionBase {
   int* h_chg = nullptr;
   int* h_flags = nullptr;
   int64_t n_product_passes = 0;
-  int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 1;
+  int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 2;
   size_t off_x = 0, off_h = 0, off_u = 0, rowbuf_bytes = 0;
   int gridX = -1000;
 
