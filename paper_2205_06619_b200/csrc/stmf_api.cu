@@ -229,7 +229,37 @@ struct Session : SessionBase {
   bool have_factors = false;
   // product caches
   DevBuf<T> t1r, t2r, t1c, t2c;
-  DevBuf<uint8_t> agr, agc;
+  DevBuf<uint8_t> agr, agc, a2r, a2c;
+  int cache_k = -1;  // >= 0: the caches are valid except for factor index cache_k
+  // row-major copies for the product passes: Urm (m x rp), Vcm (n x rp), rp = rank
+  // padded to 16 bytes, so an entry's factor rows are contiguous vector loads
+  DevBuf<T> Urm, Vcm;
+  DevBuf<int32_t> rowof_r, colof_c;  // row of each CSR entry, column of each CSC entry
+  // lines longer than long_thr entries are evaluated block-per-line (k_phaseB_long)
+  int64_t long_thr = 4096;
+  DevBuf<int32_t> long_rows, long_cols;
+  int n_long_rows = 0, n_long_cols = 0;
+  void build_long_lists() {
+    if (const char* e = getenv("STMF_LONG")) long_thr = atoll(e);
+    std::vector<int32_t> lr, lc;
+    for (int64_t i = 0; i < m; i++)
+      if (h_row_ptr[i + 1] - h_row_ptr[i] > long_thr) lr.push_back((int32_t)i);
+    for (int64_t j = 0; j < n; j++)
+      if (h_col_ptr[j + 1] - h_col_ptr[j] > long_thr) lc.push_back((int32_t)j);
+    n_long_rows = (int)lr.size();
+    n_long_cols = (int)lc.size();
+    upload(long_rows, lr);
+    upload(long_cols, lc);
+  }
+  int rp = 0;
+  void sync_factor_copies(int k) {  // k < 0: all
+    for (int l = (k < 0 ? 0 : k); l < (k < 0 ? rank : k + 1); l++) {
+      k_scatter_factor<T><<<nblk(m, 256), 256, 0, st>>>(m, rp, l, Ut.p + (size_t)l * m, Urm.p);
+      LAUNCH_CK();
+      k_scatter_factor<T><<<nblk(n, 256), 256, 0, st>>>(n, rp, l, V.p + (size_t)l * n, Vcm.p);
+      LAUNCH_CK();
+    }
+  }
   DevBuf<double> score;
   DevBuf<int32_t> colhist;
   // residuation statistics
@@ -371,6 +401,10 @@ struct Session : SessionBase {
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
+    build_long_lists();
+    rowof_r.alloc(N); colof_c.alloc(N);
+    k_line_of<<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, rowof_r.p); LAUNCH_CK();
+    k_line_of<<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, colof_c.p); LAUNCH_CK();
     // grid of the given data (binary32 mode)
     if (kExact) {
       int g = -1000;
@@ -381,6 +415,11 @@ struct Session : SessionBase {
     // caches and scratch
     Ut.alloc((size_t)rank * m); V.alloc((size_t)rank * n);
     t1r.alloc(N); t2r.alloc(N); t1c.alloc(N); t2c.alloc(N); agr.alloc(N); agc.alloc(N);
+    a2r.alloc(N); a2c.alloc(N);
+    rp = (rank + (int)(16 / sizeof(T)) - 1) / (int)(16 / sizeof(T)) * (int)(16 / sizeof(T));
+    Urm.alloc((size_t)m * rp); Vcm.alloc((size_t)n * rp);
+    CK(cudaMemsetAsync(Urm.p, 0, sizeof(T) * (size_t)m * rp, st));
+    CK(cudaMemsetAsync(Vcm.p, 0, sizeof(T) * (size_t)n * rp, st));
     score.alloc(n); colhist.alloc((size_t)n * rank);
     cm1.alloc((size_t)rank * n); cm2.alloc((size_t)rank * n); cmarg.alloc((size_t)rank * n);
     rm1.alloc((size_t)rank * m); rm2.alloc((size_t)rank * m); rmarg.alloc((size_t)rank * m);
@@ -458,9 +497,11 @@ struct Session : SessionBase {
       }
     }
     CK(cudaStreamSynchronize(st));
+    sync_factor_copies(-1);
     have_factors = true;
     cur_valid = false;
     dirty = true;
+    cache_k = -1;
     stats_dirty.assign(rank, 1);
     err_valid = false;
   }
@@ -497,18 +538,19 @@ struct Session : SessionBase {
     need_factors();
     if (dirty) {
       CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
-      k_product_csr<T><<<warps_grid(m), 256, 0, st>>>(m, n, rank, row_ptr.p, col_idx.p, Ut.p, V.p, t1r.p, t2r.p,
-                                                        agr.p);
+      // cache_k >= 0: only factor index cache_k changed since the caches were valid
+      int kk = cache_k;
+      unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
+      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
+                                           t1r.p, t2r.p, agr.p, a2r.p);
       LAUNCH_CK();
-      if (kExact) {
-        CK(cudaMemsetAsync(colhist.p, 0, sizeof(int32_t) * (size_t)n * rank, st));
-        k_product_csc_exact<T><<<warps_grid(n), 256, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p,
-                                                                t1c.p, t2c.p, agc.p, score.p, colhist.p,
-                                                                exact_limit, flags.p);
-      } else {
-        k_product_csc_warpseq<T><<<warps_grid(n), 256, 0, st>>>(m, n, rank, col_ptr.p, row_idx.p, xc.p, Ut.p, V.p,
-                                                                  t1c.p, t2c.p, agc.p, score.p, colhist.p);
-        LAUNCH_CK();
+      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
+                                           t1c.p, t2c.p, agc.p, a2c.p);
+      LAUNCH_CK();
+      k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
+                                                   !kExact, exact_limit, flags.p);
+      LAUNCH_CK();
+      if (!kExact) {
         if (n == 1) {
           DevBuf<double> col;
           col.alloc(m);
@@ -517,10 +559,10 @@ struct Session : SessionBase {
           CK(cudaStreamSynchronize(st));
         }
       }
-      LAUNCH_CK();
       n_product_passes++;
       if (kExact) check_flags();
       dirty = false;
+      cache_k = -1;
     }
     for (int k = 0; k < rank; k++) {
       if (!stats_dirty[k]) continue;
@@ -752,10 +794,13 @@ struct Session : SessionBase {
     k_chk_ilv<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bk, ubufA.p, Ut.p, chg_urf);
     LAUNCH_CK();
     int ng = (E + kEG - 1) / kEG;
-    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf};
-    SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf};
+    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf,
+                0, long_thr};
+    SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
+                0, long_thr};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
-    launch_phaseB<T>(unroll, warps_grid((m + n) * ng), st, sa, sb, E, bk, flags.p, F, exact_limit);
+    launch_phaseB<T>(unroll, warps_grid((m + n) * ng), st, sa, sb, E, bk, flags.p, F, exact_limit, long_rows.p,
+                     n_long_rows, long_cols.p, n_long_cols, nsm);
     LAUNCH_CK();
     if (profiling) CK(cudaEventRecord(ev_b1, st));
     phaseB_launches++;
@@ -853,6 +898,8 @@ struct Session : SessionBase {
     }
     CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, a, sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(V.p + (size_t)k * n, b, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
+    sync_factor_copies(k);
+    cache_k = dirty ? -1 : k;  // incremental cache update iff only this index changed
     dirty = true;
     stats_dirty[k] = 1;
   }
@@ -1086,6 +1133,8 @@ struct Session : SessionBase {
     CK(cudaStreamSynchronize(st));
     *ms = total / std::max(reps, 1);
     *errout = fx_to_double(h_acc[1], h_acc[0], F);
+    dirty = true;  // the bench overwrote the CSR caches without second-argmax tracking
+    cache_k = -1;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }

@@ -278,6 +278,152 @@ __global__ void k_product_csc_exact(int64_t m, int64_t n, int rank, const int64_
 }
 
 // ----------------------------------------------------------------------------
+// Product caches with the second argmax (a2 = an index attaining t2; 255 if
+// rank == 1).  After an accepted update only factor index k changed, so an
+// entry whose top-2 indices exclude k is updated exactly from the new k-term
+// alone; entries with k among them are recomputed over all l.  Either order
+// (lines = CSR rows or CSC columns).
+template <typename T>
+__device__ __forceinline__ void top2_full(const T* __restrict__ Ut, const T* __restrict__ V, int64_t m, int64_t n,
+                                          int rank, int64_t r, int64_t c, T& b1, T& b2, int& a1, int& a2) {
+  b1 = add_rn(Ut[r], V[c]);
+  b2 = -tinf<T>();
+  a1 = 0;
+  a2 = 255;
+  for (int l = 1; l < rank; l++) {
+    T s = add_rn(Ut[(int64_t)l * m + r], V[(int64_t)l * n + c]);
+    if (s > b1) { b2 = b1; a2 = a1; b1 = s; a1 = l; }
+    else if (s > b2) { b2 = s; a2 = l; }
+  }
+}
+
+// top-2 of U_r. + V_.c from the row-major copies Urm (m x rp) and Vcm (n x rp),
+// rp = rank padded to 16 bytes: every load is a 16-byte vector of consecutive l
+template <typename T>
+__device__ __forceinline__ void top2_vec(const T* __restrict__ Ur, const T* __restrict__ Vc, int rank, T& b1, T& b2,
+                                         int& a1, int& a2) {
+  constexpr int W = 16 / sizeof(T);
+  b1 = -tinf<T>();
+  b2 = -tinf<T>();
+  a1 = 0;
+  a2 = 255;
+  for (int l0 = 0; l0 < rank; l0 += W) {
+    T u[W], v[W];
+    if (sizeof(T) == 4) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(Ur + l0));
+      float4 b = __ldg(reinterpret_cast<const float4*>(Vc + l0));
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+      v[0] = b.x; v[1] = b.y; v[2] = b.z; v[3] = b.w;
+    } else {
+      double2 a = __ldg(reinterpret_cast<const double2*>(Ur + l0));
+      double2 b = __ldg(reinterpret_cast<const double2*>(Vc + l0));
+      u[0] = a.x; u[1] = a.y;
+      v[0] = b.x; v[1] = b.y;
+    }
+#pragma unroll
+    for (int q = 0; q < W; q++) {
+      int l = l0 + q;
+      if (l >= rank) break;
+      T s = add_rn(u[q], v[q]);
+      if (l == 0) { b1 = s; a1 = 0; }
+      else if (s > b1) { b2 = b1; a2 = a1; b1 = s; a1 = l; }
+      else if (s > b2) { b2 = s; a2 = l; }
+    }
+  }
+}
+
+// copy factor column k (contiguous in Ut / V rows) into the padded row-major copy
+template <typename T>
+__global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict__ src, T* __restrict__ dst) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < len) dst[t * rp + k] = src[t];
+}
+
+// flat over the N given entries of one order (rowof/colof: the entry's row and
+// column) -> perfectly balanced whatever the line lengths
+template <typename T>
+__global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
+                           int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
+                           const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
+                           T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+    {
+      int64_t r = rowof[p], c = colof[p];
+      T b1, b2;
+      int a1, a2;
+      bool full = k < 0;
+      if (!full) {
+        a1 = ag[p];
+        a2 = ag2[p];
+        full = a1 == k || a2 == k;
+      }
+      if (full) {
+        top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
+      } else {
+        // k held neither top-2 slot: insert its new value (lowest index on max ties)
+        T s = add_rn(Ut[(int64_t)k * m + r], V[(int64_t)k * n + c]);
+        b1 = t1[p];
+        b2 = t2[p];
+        if (s > b1 || (s == b1 && k < a1)) { b2 = b1; a2 = a1; b1 = s; a1 = k; }
+        else if (s > b2) { b2 = s; a2 = k; }
+      }
+      t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
+    }
+  }
+}
+
+// line index of every entry of a compacted layout (CSR -> row of each entry)
+__global__ void k_line_of(int64_t nlines, const int64_t* __restrict__ ptr, int32_t* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t L = w; L < nlines; L += nw)
+    for (int64_t p = ptr[L] + lane; p < ptr[L + 1]; p += 32) out[p] = (int32_t)L;
+}
+
+// column scores + TD_A histogram from the CSC caches.  fp64 (numpy order): every
+// lane folds the column's td values in row order; exact: warp sum of exact partials.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_scores(int64_t n, int rank, const int64_t* __restrict__ ptr, const T* __restrict__ xc, const T* __restrict__ t1,
+         const uint8_t* __restrict__ ag, double* __restrict__ score, int32_t* __restrict__ colhist, bool seq,
+         double exact_limit, int* __restrict__ flags) {
+  __shared__ int32_t hist[8][256];
+  int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w; c < n; c += nw) {
+    for (int l = lane; l < rank; l += 32) hist[wib][l] = 0;
+    __syncwarp();
+    double s = 0.0;
+    int64_t beg = ptr[c], end = ptr[c + 1];
+    for (int64_t base = beg; base < end; base += 32) {
+      int64_t p = base + lane;
+      double td = 0.0;
+      if (p < end) {
+        td = (double)vabs(sub_rn(xc[p], t1[p]));
+        atomicAdd(&hist[wib][ag[p]], 1);
+      }
+      if (seq) {
+        int cnt = end - base < 32 ? (int)(end - base) : 32;
+        for (int l = 0; l < cnt; l++) s = __dadd_rn(s, __shfl_sync(0xffffffffu, td, l));
+      } else {
+        s = __dadd_rn(s, td);
+      }
+    }
+    if (!seq)
+      for (int o = 16; o; o >>= 1) s = __dadd_rn(s, shfl_xor(s, o));
+    __syncwarp();
+    if (lane == 0) {
+      if (!seq && !(s < exact_limit)) atomicOr(flags, 4);
+      score[c] = s;
+    }
+    for (int l = lane; l < rank; l += 32) colhist[c * rank + l] = hist[wib][l];
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Residuation statistics for factor index k (top-2 minima + argmin).
 template <typename T>
 struct Top2 { T m1, m2; int a1; };
@@ -528,6 +674,7 @@ struct SideB {
   u64* acc;          // 2 per eval
   int* chg;          // 1 per eval
   int mode;          // 0: min + error; 1: min only (local partial); 2: error with line values from out
+  int64_t long_thr;  // lines with more entries are processed block-per-line (k_phaseB_long)
 };
 
 template <int EG, typename V>
@@ -570,6 +717,7 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
 #pragma unroll
   for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
   int64_t beg = S.ptr[L], end = S.ptr[L + 1];
+  if (end - beg > S.long_thr) return;  // a long line: k_phaseB_long
   T mn[EG];
   if (S.mode == 2) {
     // sharded F-URF second half: the line values are the all-reduced minima
@@ -674,12 +822,120 @@ k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __r
   }
 }
 
+// Long lines (more than long_thr entries: e.g. the densest rows of config 4's
+// row-clustered mask) with a whole block per (line, eval group): 8 warps stride the
+// line, the minima and error partials are combined through shared memory in a
+// fixed order.  Same arithmetic per entry as phaseB_item.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_phaseB_long(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, const int32_t* __restrict__ longA,
+              int nA, const int32_t* __restrict__ longB, int nB, int* __restrict__ flags, int F, double exact_limit) {
+  constexpr int EG = kEG;
+  __shared__ T smn[8][EG];
+  __shared__ double spart[8][EG];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int ngroups = (E + EG - 1) / EG;
+  int64_t items = (int64_t)(nA + nB) * ngroups;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    int64_t li = it / ngroups;
+    int g = (int)(it - li * ngroups);
+    const SideB<T>& S = li < nA ? A : B;
+    int64_t L = li < nA ? longA[li] : longB[li - nA];
+    int64_t nlines = S.nlines;
+    int e0 = g * EG;
+    int ne = E - e0 < EG ? E - e0 : EG;
+    const T* __restrict__ vg = S.vin + (int64_t)g * S.len_other * EG;
+    int kq[EG];
+#pragma unroll
+    for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
+    int64_t beg = S.ptr[L], end = S.ptr[L + 1];
+    T mn[EG];
+    if (S.mode == 2) {
+#pragma unroll
+      for (int q = 0; q < EG; q++) mn[q] = S.out[(int64_t)(e0 + (q < ne ? q : ne - 1)) * nlines + L];
+    } else {
+#pragma unroll
+      for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
+      for (int64_t p = beg + threadIdx.x; p < end; p += 256) {
+        T x = S.xv[p];
+        T v[EG];
+        load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+#pragma unroll
+        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < EG; q++) {
+        for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
+        if (lane == 0) smn[wid][q] = mn[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < EG; q++) {
+        T v = smn[0][q];
+        for (int w = 1; w < 8; w++) v = vmin(v, smn[w][q]);
+        mn[q] = v;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < ne) {
+      int q = threadIdx.x;
+      T w = lane_pick<EG>(mn, q);
+      int kl = lane_pick<EG>(kq, q);
+      if (S.mode != 2) S.out[(int64_t)(e0 + q) * nlines + L] = w;
+      if (S.mode != 1 && w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + q] = 1;
+    }
+    if (S.mode == 1) continue;
+    double part[EG];
+#pragma unroll
+    for (int q = 0; q < EG; q++) part[q] = 0.0;
+    for (int64_t p = beg + threadIdx.x; p < end; p += 256) {
+      T x = S.xv[p];
+      T a1 = S.t1[p], a2 = S.t2[p];
+      int a = S.ag[p];
+      T v[EG];
+      load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+#pragma unroll
+      for (int q = 0; q < EG; q++) {
+        T Q = (a == kq[q]) ? a2 : a1;
+        T pm = vmax(Q, add_rn(mn[q], v[q]));
+        part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x, pm)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EG; q++) {
+      for (int o = 16; o; o >>= 1) part[q] = __dadd_rn(part[q], shfl_xor(part[q], o));
+      if (lane == 0) spart[wid][q] = part[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < ne) {
+      int q = threadIdx.x;
+      double pv = spart[0][q];
+      for (int w = 1; w < 8; w++) pv = __dadd_rn(pv, spart[w][q]);
+      int fl = 0;
+      if (!(pv < exact_limit)) fl |= 4;
+      u64 hi, lo;
+      fx_from_double(pv, F, hi, lo, fl);
+      fx_atomic_add(S.acc + 2 * (e0 + q), hi, lo);
+      if (fl & 6) atomicOr(flags, fl);
+    }
+    __syncthreads();
+  }
+}
+
+// lines longer than the sides' long_thr are listed in longA / longB and handled by
+// k_phaseB_long (a block per line) — call sites set long_thr consistently
 template <typename T>
 inline void launch_phaseB(int unroll, unsigned grid, cudaStream_t st, const SideB<T>& A, const SideB<T>& B, int E,
-                          const int32_t* ek, int* flags, int F, double exact_limit) {
+                          const int32_t* ek, int* flags, int F, double exact_limit, const int32_t* longA = nullptr,
+                          int nA = 0, const int32_t* longB = nullptr, int nB = 0, int nsm = 148) {
   if (unroll >= 4) k_phaseB<T, 4><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
   else if (unroll == 2) k_phaseB<T, 2><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
   else k_phaseB<T, 1><<<grid, 256, 0, st>>>(A, B, E, ek, flags, F, exact_limit);
+  if (nA + nB > 0) {
+    int64_t items = (int64_t)(nA + nB) * ((E + kEG - 1) / kEG);
+    unsigned g = (unsigned)std::min<int64_t>(items, (int64_t)nsm * 8);
+    k_phaseB_long<T><<<g, 256, 0, st>>>(A, B, E, ek, longA, nA, longB, nB, flags, F, exact_limit);
+  }
 }
 
 // Exact/bounded objective of an explicit state: entries' residual |x - max(Q^k, a_r + b_c)|

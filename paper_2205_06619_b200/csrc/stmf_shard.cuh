@@ -279,7 +279,11 @@ struct Shard {
   int64_t max_rownnz = 0;
   DevBuf<T> Ut, V;
   DevBuf<T> t1r, t2r, t1c, t2c;
-  DevBuf<uint8_t> agr, agc;
+  DevBuf<uint8_t> agr, agc, a2r, a2c;
+  DevBuf<T> Urm, Vcm;  // row-major factor copies (ml x rp, n x rp) for the product passes
+  DevBuf<int32_t> rowof_r, colof_c;
+  DevBuf<int32_t> long_rows, long_cols;  // lines evaluated block-per-line
+  int n_long_rows = 0, n_long_cols = 0;
   DevBuf<double> score;
   DevBuf<int64_t> scorefx;
   DevBuf<int32_t> colhist;
@@ -313,6 +317,17 @@ struct ShardGroup : SessionBase {
   int F = 0;
   double exact_limit = INFINITY;
   bool dirty = true, err_valid = false, have_factors = false;
+  int cache_k = -1;  // >= 0: caches valid except for factor index cache_k
+  int rp = 4;
+  void sync_factor_copies(int k) {  // k < 0: all
+    for (auto& s : sh)
+      for (int l = (k < 0 ? 0 : k); l < (k < 0 ? rank : k + 1); l++) {
+        k_scatter_factor<T><<<nblk(s->ml, 256), 256, 0, st>>>(s->ml, rp, l, s->Ut.p + (size_t)l * s->ml, s->Urm.p);
+        LAUNCH_CK();
+        k_scatter_factor<T><<<nblk(n, 256), 256, 0, st>>>(n, rp, l, s->V.p + (size_t)l * n, s->Vcm.p);
+        LAUNCH_CK();
+      }
+  }
   std::vector<char> stats_dirty;
   double err = 0;
   u64* h_acc = nullptr;
@@ -321,6 +336,7 @@ struct ShardGroup : SessionBase {
   int* h_flags = nullptr;
   int64_t n_product_passes = 0;
   int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 2;
+  int64_t long_thr = getenv("STMF_LONG") ? atoll(getenv("STMF_LONG")) : 4096;
   size_t off_x = 0, off_h = 0, off_u = 0, rowbuf_bytes = 0;
   int gridX = -1000;
 
@@ -426,12 +442,38 @@ struct ShardGroup : SessionBase {
     s.col_idx.alloc(Nl); s.row_idx.alloc(Nl); s.xr.alloc(Nl); s.xc.alloc(Nl);
     k_fill_csr<T><<<nblk(ml * 32, 256), 256, 0, st>>>(ml, n, dX.p, dM.p, s.row_ptr.p, s.col_idx.p, s.xr.p);
     LAUNCH_CK();
+    {
+      std::vector<int64_t> hcp(n + 1);
+      CK(cudaMemcpyAsync(hcp.data(), s.col_ptr.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<int32_t> lr, lc;
+      for (int64_t i = 0; i < ml; i++)
+        if (s.h_row_ptr[i + 1] - s.h_row_ptr[i] > long_thr) lr.push_back((int32_t)i);
+      for (int64_t j = 0; j < n; j++)
+        if (hcp[j + 1] - hcp[j] > long_thr) lc.push_back((int32_t)j);
+      s.n_long_rows = (int)lr.size();
+      s.n_long_cols = (int)lc.size();
+      s.long_rows.alloc(std::max<size_t>(lr.size(), 1));
+      s.long_cols.alloc(std::max<size_t>(lc.size(), 1));
+      if (!lr.empty()) CK(cudaMemcpy(s.long_rows.p, lr.data(), 4 * lr.size(), cudaMemcpyHostToDevice));
+      if (!lc.empty()) CK(cudaMemcpy(s.long_cols.p, lc.data(), 4 * lc.size(), cudaMemcpyHostToDevice));
+    }
+    s.rowof_r.alloc(Nl); s.colof_c.alloc(Nl);
+    k_line_of<<<warps_grid(ml), 256, 0, st>>>(ml, s.row_ptr.p, s.rowof_r.p);
+    LAUNCH_CK();
+    k_line_of<<<warps_grid(n), 256, 0, st>>>(n, s.col_ptr.p, s.colof_c.p);
+    LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(ml, n, dX.p, dM.p, s.col_ptr.p, s.row_idx.p, s.xc.p);
     LAUNCH_CK();
     for (int64_t a = 0; a < ml * n; a++)
       if (mask[a]) gridX = std::max(gridX, f32_grid((float)X[a]));
     s.Ut.alloc((size_t)rank * ml); s.V.alloc((size_t)rank * n);
     s.t1r.alloc(Nl); s.t2r.alloc(Nl); s.agr.alloc(Nl); s.t1c.alloc(Nl); s.t2c.alloc(Nl); s.agc.alloc(Nl);
+    s.a2r.alloc(Nl); s.a2c.alloc(Nl);
+    rp = (rank + 3) / 4 * 4;
+    s.Urm.alloc((size_t)ml * rp); s.Vcm.alloc((size_t)n * rp);
+    CK(cudaMemsetAsync(s.Urm.p, 0, sizeof(T) * (size_t)ml * rp, st));
+    CK(cudaMemsetAsync(s.Vcm.p, 0, sizeof(T) * (size_t)n * rp, st));
     s.score.alloc(n); s.scorefx.alloc(n); s.colhist.alloc((size_t)n * rank);
     s.cm1.alloc((size_t)rank * n); s.cm2.alloc((size_t)rank * n); s.cmarg.alloc((size_t)rank * n);
     s.rm1.alloc((size_t)rank * ml); s.rm2.alloc((size_t)rank * ml); s.rmarg.alloc((size_t)rank * ml);
@@ -497,8 +539,10 @@ struct ShardGroup : SessionBase {
       comm->min_f32(reinterpret_cast<std::vector<float*>&>(vp), (size_t)rank * n, st);
     }
     CK(cudaStreamSynchronize(st));
+    sync_factor_copies(-1);
     have_factors = true;
     dirty = true;
+    cache_k = -1;
     stats_dirty.assign(rank, 1);
     err_valid = false;
   }
@@ -538,13 +582,15 @@ struct ShardGroup : SessionBase {
       for (auto& sp : sh) {
         Shard<T>& s = *sp;
         CK(cudaMemsetAsync(s.flags.p, 0, sizeof(int), st));
-        k_product_csr<T><<<warps_grid(s.ml), 256, 0, st>>>(s.ml, n, rank, s.row_ptr.p, s.col_idx.p, s.Ut.p, s.V.p,
-                                                             s.t1r.p, s.t2r.p, s.agr.p);
+        unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(s.Nl, 256), (int64_t)nsm * 16));
+        k_product2<T><<<gflat, 256, 0, st>>>(s.Nl, s.rowof_r.p, s.col_idx.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
+                                             s.Vcm.p, rp, cache_k, s.t1r.p, s.t2r.p, s.agr.p, s.a2r.p);
         LAUNCH_CK();
-        CK(cudaMemsetAsync(s.colhist.p, 0, sizeof(int32_t) * (size_t)n * rank, st));
-        k_product_csc_exact<T><<<warps_grid(n), 256, 0, st>>>(s.ml, n, rank, s.col_ptr.p, s.row_idx.p, s.xc.p,
-                                                                s.Ut.p, s.V.p, s.t1c.p, s.t2c.p, s.agc.p, s.score.p,
-                                                                s.colhist.p, exact_limit, s.flags.p);
+        k_product2<T><<<gflat, 256, 0, st>>>(s.Nl, s.row_idx.p, s.colof_c.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
+                                             s.Vcm.p, rp, cache_k, s.t1c.p, s.t2c.p, s.agc.p, s.a2c.p);
+        LAUNCH_CK();
+        k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, s.col_ptr.p, s.xc.p, s.t1c.p, s.agc.p, s.score.p,
+                                                     s.colhist.p, false, exact_limit, s.flags.p);
         LAUNCH_CK();
         k_score_to_fx<<<nblk(n, 256), 256, 0, st>>>(n, s.score.p, s.scorefx.p, std::ldexp(1.0, F));
         LAUNCH_CK();
@@ -560,6 +606,7 @@ struct ShardGroup : SessionBase {
       check_flags();
       n_product_passes++;
       dirty = false;
+      cache_k = -1;
     }
     for (int k = 0; k < rank; k++) {
       if (!stats_dirty[k]) continue;
@@ -684,10 +731,11 @@ struct ShardGroup : SessionBase {
       k_chk_ilv<T><<<nblk(G8 * s.ml, 256), 256, 0, st>>>(s.ml, E, bk, s.ubufA.p, s.Ut.p, s.chg.p + E);
       LAUNCH_CK();
       SideB<T> sa{s.ml, s.row_ptr.p, s.col_idx.p, s.xr.p, s.t1r.p, s.t2r.p, s.agr.p, s.vbuf.p, n, s.Ut.p, s.ubufB.p,
-                  s.acc.p, s.chg.p, 0};
+                  s.acc.p, s.chg.p, 0, long_thr};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
-                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 1};
-      launch_phaseB<T>(unroll, warps_grid((s.ml + n) * ng), st, sa, sb, E, bk, s.flags.p, F, exact_limit);
+                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 1, long_thr};
+      launch_phaseB<T>(unroll, warps_grid((s.ml + n) * ng), st, sa, sb, E, bk, s.flags.p, F, exact_limit,
+                       s.long_rows.p, s.n_long_rows, s.long_cols.p, s.n_long_cols, nsm);
       LAUNCH_CK();
     }
     // F-URF: v''_c = min over ALL rows -> all-reduce MIN of the local column minima
@@ -697,10 +745,11 @@ struct ShardGroup : SessionBase {
       Shard<T>& s = *sp;
       const int32_t* bk = s.ck.p + t0;
       SideB<T> none{0, s.row_ptr.p, s.col_idx.p, s.xr.p, s.t1r.p, s.t2r.p, s.agr.p, s.vbuf.p, n, s.Ut.p, s.ubufB.p,
-                    s.acc.p, s.chg.p, 0};
+                    s.acc.p, s.chg.p, 0, long_thr};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
-                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 2};
-      launch_phaseB<T>(unroll, warps_grid(n * ng), st, none, sb, E, bk, s.flags.p, F, exact_limit);
+                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 2, long_thr};
+      launch_phaseB<T>(unroll, warps_grid(n * ng), st, none, sb, E, bk, s.flags.p, F, exact_limit, nullptr, 0,
+                       s.long_cols.p, s.n_long_cols, nsm);
       LAUNCH_CK();
     }
     reduce_acc(2 * E);
@@ -729,6 +778,8 @@ struct ShardGroup : SessionBase {
       CK(cudaMemcpyAsync(s.Ut.p + (size_t)k * s.ml, a, sizeof(T) * s.ml, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(s.V.p + (size_t)k * n, b, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
     }
+    sync_factor_copies(k);
+    cache_k = dirty ? -1 : k;
     dirty = true;
     stats_dirty[k] = 1;
   }

@@ -138,6 +138,30 @@ def test_f64_fit_matches_restatement_lognormal():
     assert counts["attempts"] == ref["attempts"]
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_block_per_line_path_matches_restatement(monkeypatch, dtype):
+    """Force every line with > 16 entries through the block-per-line phase-B kernel."""
+    monkeypatch.setenv("STMF_LONG", "16")
+    work, U0 = _f32_case(7, 40, 90, 4, 0.5)
+    X = work.values.astype(dtype)
+    U0 = U0.astype(dtype)
+    V0 = np.stack([oracle.residuate_row(X, work.mask, U0[:, k]) for k in range(4)])
+    ref = oracle.fit(X, work.mask, U0, V0, budget_sweeps=2, epsilon=0.0)
+    with _ext.Session(X, work.mask, 4) as s:
+        s.set_factors(U0)
+        tt, te, c = s.run(budget_sweeps=2, epsilon=0.0)
+        U, V = s.get_factors()
+    assert np.array_equal(te, ref["traj_err"]) and np.array_equal(U, ref["U"]) and np.array_equal(V, ref["V"])
+    if dtype == np.float32:
+        g = _ext.Session.sim_group(X, work.mask, 4, 3)
+        try:
+            g.set_factors(U0)
+            tt, te2, c2 = g.run(budget_sweeps=2, epsilon=0.0)
+        finally:
+            g.close()
+        assert np.array_equal(te2, ref["traj_err"])
+
+
 def test_attempt_commit_semantics(fits):
     c = fit_case(fits, "s2")
     X, M = c["work_X"], c["work_M"]
