@@ -237,6 +237,8 @@ struct Session : SessionBase {
   DevBuf<int32_t> rowof_r, colof_c;  // row of each CSR entry, column of each CSC entry
   // lines longer than long_thr entries are evaluated block-per-line (k_phaseB_long)
   int64_t long_thr = 4096;
+  // phase-B item order: group-major when both orders' entry data fit comfortably in L2
+  int group_major = 0;
   DevBuf<int32_t> long_rows, long_cols;
   int n_long_rows = 0, n_long_cols = 0;
   void build_long_lists() {
@@ -402,6 +404,15 @@ struct Session : SessionBase {
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(m, n, dX.p, dM.p, col_ptr.p, row_idx.p, xc.p); LAUNCH_CK();
     build_long_lists();
+    {
+      // x, idx, t1, t2, ag per entry in each order
+      double entry_bytes = 2.0 * (double)N * (3 * sizeof(T) + 4 + 1);
+      group_major = entry_bytes < 0.5 * (double)prop.l2CacheSize ? 1 : 0;
+      if (const char* e = getenv("STMF_GROUP_MAJOR")) group_major = atoi(e);
+      CK(cudaFuncSetAttribute(k_phaseB<T, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+      CK(cudaFuncSetAttribute(k_phaseB<T, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+      CK(cudaFuncSetAttribute(k_phaseB<T, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    }
     rowof_r.alloc(N); colof_c.alloc(N);
     k_line_of<<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, rowof_r.p); LAUNCH_CK();
     k_line_of<<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, colof_c.p); LAUNCH_CK();
@@ -795,9 +806,9 @@ struct Session : SessionBase {
     LAUNCH_CK();
     int ng = (E + kEG - 1) / kEG;
     SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf,
-                0, long_thr};
+                0, long_thr, group_major};
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
-                0, long_thr};
+                0, long_thr, group_major};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
     launch_phaseB<T>(unroll, warps_grid((m + n) * ng), st, sa, sb, E, bk, flags.p, F, exact_limit, long_rows.p,
                      n_long_rows, long_cols.p, n_long_cols, nsm);

@@ -29,9 +29,12 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+// fp64 min/max as compare-select: no NaN can occur on the path (given entries and
+// factors are finite; +-inf only as identities), so IEEE fmin's NaN handling is
+// dead weight (DSETP + 2 selects instead of DSETP.MIN + SEL + LOP3 + FSEL)
+__device__ __forceinline__ double vmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
-__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return b > a ? b : a; }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double vabs(double a) { return fabs(a); }
 __device__ __forceinline__ float vabs(float a) { return fabsf(a); }
@@ -675,6 +678,8 @@ struct SideB {
   int* chg;          // 1 per eval
   int mode;          // 0: min + error; 1: min only (local partial); 2: error with line values from out
   int64_t long_thr;  // lines with more entries are processed block-per-line (k_phaseB_long)
+  int group_major;   // item order: 1 = eval-group major (entry data L2-resident: vin block
+                     // stays hot in L1), 0 = line major (entry data streamed once per batch)
 };
 
 template <int EG, typename V>
@@ -707,9 +712,17 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   int64_t nlines = S.nlines;
   int ngroups = (E + EG - 1) / EG;
   // line-major: the warps of one line (one per eval group) run together, so the
-  // line's entries are read from DRAM once per batch; the small vin blocks stay in L2
-  int64_t L = it / ngroups;
-  int g = (int)(it - L * ngroups);
+  // line's entries are read from DRAM once per batch; the small vin blocks stay in L2.
+  // group-major: concurrent warps share one group's vin block (L1-resident).
+  int64_t L;
+  int g;
+  if (S.group_major) {
+    g = (int)(it / nlines);
+    L = it - (int64_t)g * nlines;
+  } else {
+    L = it / ngroups;
+    g = (int)(it - L * ngroups);
+  }
   int e0 = g * EG;
   int ne = E - e0 < EG ? E - e0 : EG;
   const T* __restrict__ vg = S.vin + (int64_t)g * S.len_other * EG;
@@ -808,7 +821,7 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
 // UNR = entries per lane per loop iteration (memory-level parallelism vs registers)
 template <typename T, int UNR>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 || UNR > 2) ? 2 : 3)
+__global__ void __launch_bounds__(256, UNR > 2 ? 2 : (sizeof(T) == 8 && UNR > 1 ? 2 : 3))
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
          double exact_limit) {
   int lane = threadIdx.x & 31;

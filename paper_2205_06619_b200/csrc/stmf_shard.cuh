@@ -337,6 +337,7 @@ struct ShardGroup : SessionBase {
   int64_t n_product_passes = 0;
   int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 2;
   int64_t long_thr = getenv("STMF_LONG") ? atoll(getenv("STMF_LONG")) : 4096;
+  int group_major = 0;
   size_t off_x = 0, off_h = 0, off_u = 0, rowbuf_bytes = 0;
   int gridX = -1000;
 
@@ -408,6 +409,12 @@ struct ShardGroup : SessionBase {
     CK(cudaMallocHost(&h_limbs, sizeof(int64_t) * 6 * Emax));
     CK(cudaMallocHost(&h_chg, sizeof(int) * 2 * Emax));
     CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
+    {
+      double nl = 0;
+      for (auto& s : sh) nl += (double)s->Nl;
+      group_major = 2.0 * nl * (3 * sizeof(T) + 5) < 0.5 * (double)prop.l2CacheSize ? 1 : 0;
+      if (const char* e = getenv("STMF_GROUP_MAJOR")) group_major = atoi(e);
+    }
     stats_dirty.assign(rank, 1);
     CK(cudaStreamSynchronize(st));
   }
@@ -731,9 +738,9 @@ struct ShardGroup : SessionBase {
       k_chk_ilv<T><<<nblk(G8 * s.ml, 256), 256, 0, st>>>(s.ml, E, bk, s.ubufA.p, s.Ut.p, s.chg.p + E);
       LAUNCH_CK();
       SideB<T> sa{s.ml, s.row_ptr.p, s.col_idx.p, s.xr.p, s.t1r.p, s.t2r.p, s.agr.p, s.vbuf.p, n, s.Ut.p, s.ubufB.p,
-                  s.acc.p, s.chg.p, 0, long_thr};
+                  s.acc.p, s.chg.p, 0, long_thr, group_major};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
-                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 1, long_thr};
+                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 1, long_thr, group_major};
       launch_phaseB<T>(unroll, warps_grid((s.ml + n) * ng), st, sa, sb, E, bk, s.flags.p, F, exact_limit,
                        s.long_rows.p, s.n_long_rows, s.long_cols.p, s.n_long_cols, nsm);
       LAUNCH_CK();
@@ -745,9 +752,9 @@ struct ShardGroup : SessionBase {
       Shard<T>& s = *sp;
       const int32_t* bk = s.ck.p + t0;
       SideB<T> none{0, s.row_ptr.p, s.col_idx.p, s.xr.p, s.t1r.p, s.t2r.p, s.agr.p, s.vbuf.p, n, s.Ut.p, s.ubufB.p,
-                    s.acc.p, s.chg.p, 0, long_thr};
+                    s.acc.p, s.chg.p, 0, long_thr, group_major};
       SideB<T> sb{n, s.col_ptr.p, s.row_idx.p, s.xc.p, s.t1c.p, s.t2c.p, s.agc.p, s.ubufA.p, s.ml, s.V.p, s.vbufB.p,
-                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 2, long_thr};
+                  s.acc.p + 2 * (size_t)E, s.chg.p + E, 2, long_thr, group_major};
       launch_phaseB<T>(unroll, warps_grid(n * ng), st, none, sb, E, bk, s.flags.p, F, exact_limit, nullptr, 0,
                        s.long_cols.p, s.n_long_cols, nsm);
       LAUNCH_CK();

@@ -99,9 +99,12 @@ def _f32_case(seed, m, n, r, frac):
     return work, U0
 
 
+@pytest.mark.parametrize("order", ["0", "1"])
 @pytest.mark.parametrize("seed,m,n,r,frac,sweeps", [(1, 30, 50, 3, 0.3, 4), (2, 64, 200, 5, 0.7, 2),
                                                      (3, 120, 90, 10, 0.5, 1)])
-def test_f32_fit_matches_restatement(seed, m, n, r, frac, sweeps):
+def test_f32_fit_matches_restatement(monkeypatch, order, seed, m, n, r, frac, sweeps):
+    """Both phase-B item orders (line-major / group-major, STMF_GROUP_MAJOR)."""
+    monkeypatch.setenv("STMF_GROUP_MAJOR", order)
     work, U0 = _f32_case(seed, m, n, r, frac)
     with _ext.Session(work.values, work.mask, r) as s:
         s.set_factors(U0)
@@ -119,8 +122,10 @@ def test_f32_fit_matches_restatement(seed, m, n, r, frac, sweeps):
     assert te[-1] == math.fsum(np.abs(work.values[M] - P[M]).astype(np.float64).tolist())
 
 
-def test_f64_fit_matches_restatement_lognormal():
+@pytest.mark.parametrize("order", ["0", "1"])
+def test_f64_fit_matches_restatement_lognormal(monkeypatch, order):
     """A reduced config-2 shape (log2(1+lognormal), 50% hidden) vs the oracle."""
+    monkeypatch.setenv("STMF_GROUP_MAJOR", order)
     rng = np.random.default_rng(5)
     X = np.log2(1 + rng.lognormal(0, 1, (60, 140)))
     from paper_2205_06619_b200 import gen
