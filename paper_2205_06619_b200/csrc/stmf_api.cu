@@ -287,6 +287,7 @@ struct Session : SessionBase {
   DevBuf<double> pwval;
   DevBuf<int64_t> pw_loff;
   DevBuf<int32_t> pw_llen, pw_lnode, pw_left, pw_right, pw_lvloff, pw_lvlnodes;
+  DevBuf<int4> pw_ops;  // internal nodes in level order: {node, left, right, 0}
   PWTree pw;
   DevBuf<uint8_t> cubtmp;
   size_t cubtmp_bytes = 0;
@@ -412,6 +413,8 @@ struct Session : SessionBase {
       CK(cudaFuncSetAttribute(k_phaseB<T, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
       CK(cudaFuncSetAttribute(k_phaseB<T, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
       CK(cudaFuncSetAttribute(k_phaseB<T, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+      CK(cudaFuncSetAttribute(k_pw_combine_multi_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kCombineSmem));
     }
     rowof_r.alloc(N); colof_c.alloc(N);
     k_line_of<<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, rowof_r.p); LAUNCH_CK();
@@ -454,6 +457,15 @@ struct Session : SessionBase {
       upload(pw_loff, pw.loff); upload(pw_llen, pw.llen); upload(pw_lnode, pw.lnode);
       upload(pw_left, pw.left); upload(pw_right, pw.right);
       upload(pw_lvloff, pw.lvl_off); upload(pw_lvlnodes, pw.lvl_nodes);
+      {
+        std::vector<int4> ops(pw.lvl_nodes.size());
+        for (size_t t = 0; t < ops.size(); t++) {
+          int nd = pw.lvl_nodes[t];
+          ops[t] = make_int4(nd, pw.left[nd], pw.right[nd], 0);
+        }
+        pw_ops.alloc(std::max<size_t>(ops.size(), 1));
+        if (!ops.empty()) CK(cudaMemcpy(pw_ops.p, ops.data(), sizeof(int4) * ops.size(), cudaMemcpyHostToDevice));
+      }
       int depth = 26 + (int)std::ceil(std::log2((double)N + 1));
       beta_rel = 1.01 * depth * std::ldexp(1.0, -53);
     }
@@ -609,6 +621,7 @@ struct Session : SessionBase {
   // delta path (<= kDeltaCap changed entries vs the current state) runs device-gated
   // for every slot; slots whose change set is larger are redone with a full sort.
   static constexpr int kSlots = 8;
+  static constexpr size_t kCombineSmem = 160 * 1024;
   struct Slot {
     DevBuf<u64> res, sorted, olds, news;
     DevBuf<int> dcount;
@@ -616,6 +629,7 @@ struct Session : SessionBase {
     DevBuf<double> pw;
     const T* ap = nullptr;
     const T* bp = nullptr;
+    int as = 1, bs = 1;  // element strides of ap / bp (EGP: one eval of a planar buffer)
     int k = 0;
   };
   std::vector<Slot> slots;
@@ -624,11 +638,13 @@ struct Session : SessionBase {
   RepSlot<T>* h_rep = nullptr;
   DevBuf<RepSlot<T>> d_rep;
   DevBuf<int> d_dcounts;
+  DevBuf<double> d_pwout;
 
   void alloc_slots() {
     CK(cudaMallocHost(&h_rep, sizeof(RepSlot<T>) * kSlots));
     d_rep.alloc(kSlots);
     d_dcounts.alloc(kSlots);
+    d_pwout.alloc(kSlots);
     slots.resize(kSlots);
     for (auto& s : slots) {
       s.res.alloc(N); s.sorted.alloc(N); s.olds.alloc(kDeltaCap); s.news.alloc(kDeltaCap); s.dcount.alloc(1);
@@ -659,51 +675,21 @@ struct Session : SessionBase {
   // replicas of slots[0, count) (ap, bp, k set) -> h_pwv[s]
   void replicas(int count) {
     bool delta = cur_valid;
-    n_escalations += count;
-    if (delta) {
-      // one launch per step for the whole round (slot = blockIdx.y)
-      for (int i = 0; i < count; i++) {
-        Slot& s = slots[i];
-        h_rep[i] = RepSlot<T>{s.k, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p, d_dcounts.p + i, s.pw.p};
-      }
-      CK(cudaMemcpyAsync(d_rep.p, h_rep, sizeof(RepSlot<T>) * count, cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(d_dcounts.p, 0, sizeof(int) * count, st));
-      dim3 g1(warps_grid(m), count);
-      k_residuals_delta_multi<T><<<g1, 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, res_cur.p,
-                                                      d_rep.p);
-      LAUNCH_CK();
-      k_sort_delta_multi<T><<<dim3(2, count), 1024, 0, st>>>(d_rep.p);
-      LAUNCH_CK();
-      k_merge_delta_multi<T><<<dim3(nblk(N + kDeltaCap, 256), count), 256, 0, st>>>(N, S_cur.p, d_rep.p);
-      LAUNCH_CK();
-      int nl = (int)pw.loff.size();
-      k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), count), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
-                                                                                     pw_lnode.p, d_rep.p);
-      LAUNCH_CK();
-      if (pw.H > 0) {
-        k_pw_combine_multi<T><<<dim3(1, count), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
-                                                                pw_right.p, d_rep.p);
-        LAUNCH_CK();
-      }
-      CK(cudaMemcpyAsync(h_dcount, d_dcounts.p, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
-      for (int i = 0; i < count; i++)
-        CK(cudaMemcpyAsync(h_pwv + i, slots[i].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    }
+    enqueue_replicas(count);
     for (int i = 0; i < count && !delta; i++) {
       Slot& s = slots[i];
-      {
-        k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, s.k, s.ap,
-                                                        s.bp, s.res.p);
-        LAUNCH_CK();
-        full_sort(s);
-        h_dcount[i] = 0;
-      }
+      k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, s.k, s.ap,
+                                                      s.as, s.bp, s.bs, s.res.p);
+      LAUNCH_CK();
+      full_sort(s);
+      h_dcount[i] = 0;
       pw_sum(s);
       CK(cudaMemcpyAsync(h_pwv + i, s.pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
     bool redo = false;
     for (int i = 0; i < count; i++) {
+      if (dhist_on) dhist[std::min(13, 32 - __builtin_clz((unsigned)h_dcount[i] | 1))]++;
       if (delta && h_dcount[i] == 0) n_zero_delta++;
       if (!delta || h_dcount[i] <= kDeltaCap) {
         n_delta_replicas += delta;
@@ -717,8 +703,90 @@ struct Session : SessionBase {
     if (redo) CK(cudaStreamSynchronize(st));
   }
 
+  // the delta replica steps of slots[0, count) on the stream, results copied to
+  // h_dcount / h_pwv without a host sync (no-op unless the current state is valid)
+  void enqueue_replicas(int count) {
+    bool delta = cur_valid;
+    n_escalations += count;
+    if (delta) {
+      // one launch per step for the whole round (slot = blockIdx.y)
+      for (int i = 0; i < count; i++) {
+        Slot& s = slots[i];
+        h_rep[i] = RepSlot<T>{s.k, s.as, s.bs, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p,
+                              d_dcounts.p + i, s.pw.p, d_pwout.p + i};
+      }
+      CK(cudaMemcpyAsync(d_rep.p, h_rep, sizeof(RepSlot<T>) * count, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(d_dcounts.p, 0, sizeof(int) * count, st));
+      k_residuals_delta_multi<T><<<dim3(nblk(N, 256), count), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p,
+                                                                              t2r.p, agr.p, res_cur.p, d_rep.p);
+      LAUNCH_CK();
+      k_sort_delta_multi<T><<<dim3(2, count), kSortThreads, 0, st>>>(d_rep.p);
+      LAUNCH_CK();
+      unsigned mt = (unsigned)((N + kMergeTile - 1) / kMergeTile);
+      k_merge_delta_multi<T><<<dim3(mt, count), 256, 0, st>>>(N, S_cur.p, d_rep.p);
+      LAUNCH_CK();
+      int nl = (int)pw.loff.size();
+      k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), count), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
+                                                                                     pw_lnode.p, d_rep.p);
+      LAUNCH_CK();
+      if (pw.H > 0) {
+        int nops = (int)pw.lvl_nodes.size();
+        size_t sm = sizeof(double) * (size_t)((pw.nnodes + 1) & ~1) + sizeof(int4) * (size_t)nops +
+                    sizeof(int) * (size_t)(pw.H + 1);
+        if (sm <= kCombineSmem)
+          k_pw_combine_multi_smem<T><<<dim3(1, count), 1024, sm, st>>>(pw.H, pw.nnodes, nops, pw_lvloff.p, pw_ops.p,
+                                                                       d_rep.p);
+        else
+          k_pw_combine_multi<T><<<dim3(1, count), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
+                                                                  pw_right.p, d_rep.p);
+        LAUNCH_CK();
+      }
+      CK(cudaMemcpyAsync(h_dcount, d_dcounts.p, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_pwv, d_pwout.p, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    }
+  }
+
+  // ---- deferred accept (fp64) ------------------------------------------------------
+  // A certain accept (A + margin < err) is committed without waiting for its numpy
+  // replica: the replica runs on the stream and its value becomes err at the next
+  // point that needs err (the next decision, a sweep boundary, the end of the run).
+  bool err_pending = false;
+  double* pend_te = nullptr;  // trajectory slot to fill with the resolved value
+  int64_t n_deferred = 0;
+
+  void resolve_err() {
+    if (!err_pending) return;
+    CK(cudaStreamSynchronize(st));
+    double fr = h_pwv[0];
+    if (h_dcount[0] > kDeltaCap) {
+      // too many changed entries for the delta merge: sort the adopted residuals
+      size_t bytes = cubtmp_bytes;
+      CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res_cur.p, S_cur.p, (int64_t)N, 0, 63, st));
+      g_cub_calls++;
+      int nl = (int)pw.loff.size();
+      k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, S_cur.p,
+                                                              slots[0].pw.p);
+      LAUNCH_CK();
+      if (pw.H > 0) {
+        k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, slots[0].pw.p);
+        LAUNCH_CK();
+      }
+      CK(cudaMemcpyAsync(h_pwv, slots[0].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      fr = h_pwv[0];
+    } else {
+      n_delta_replicas++;
+      if (h_dcount[0] == 0) n_zero_delta++;
+    }
+    if (!(fr < err)) fail(STMF_ERR_NUMERIC, "decision bound violated: replica=%.17g err=%.17g", fr, err);
+    err = fr;
+    if (pend_te) *pend_te = fr;
+    pend_te = nullptr;
+    err_pending = false;
+  }
+
   double replica1(int k, const T* a, const T* b) {
-    slots[0].k = k; slots[0].ap = a; slots[0].bp = b;
+    slots[0].k = k; slots[0].ap = a; slots[0].bp = b; slots[0].as = slots[0].bs = 1;
     replicas(1);
     return h_pwv[0];
   }
@@ -734,20 +802,22 @@ struct Session : SessionBase {
   void set_slot_eval(int s, int op, int q, int k) {
     Slot& S = slots[s];
     S.k = k;
+    constexpr int EGP = Ilv<T>::EGP;
     if (op == 0) {
       S.ap = ubufB.p + (size_t)q * m;
-      k_deinterleave<T><<<nblk(n, 256), 256, 0, st>>>(n, q, vbuf.p, S.b.p);
-      LAUNCH_CK();
-      S.bp = S.b.p;
+      S.as = 1;
+      S.bp = vbuf.p + ilv_index<T>(q, 0, n);
+      S.bs = EGP;
     } else {
-      k_deinterleave<T><<<nblk(m, 256), 256, 0, st>>>(m, q, ubufA.p, S.a.p);
-      LAUNCH_CK();
-      S.ap = S.a.p;
+      S.ap = ubufA.p + ilv_index<T>(q, 0, m);
+      S.as = EGP;
       S.bp = vbufB.p + (size_t)q * n;
+      S.bs = 1;
     }
   }
 
   double objective() override {
+    resolve_err();
     ensure_caches();
     if (!err_valid) {
       err = state_objective(0, Ut.p, V.p);
@@ -853,7 +923,9 @@ struct Session : SessionBase {
   // the first eval with f < err wins.  Returns the winner's order index or -1 and
   // commits it.  fp64: evals whose bound straddles err, and the first certain
   // accept (its numpy value becomes err), are replicated in rounds of kSlots.
-  int decide_batch(int E, const std::vector<int>& hk, double* fwin) {
+  int decide_batch(int E, const std::vector<int>& hk, double* fwin, bool* deferred = nullptr) {
+    resolve_err();
+    if (deferred) *deferred = false;
     int pos = 0;
     while (pos < 2 * E) {
       struct Req { int ev, q, op; bool certain; };
@@ -875,6 +947,16 @@ struct Session : SessionBase {
         if (A - mg >= err) continue;  // certainly not below err
         chunk.push_back({scan, q, op, A + mg < err});
         if (A + mg < err) { scan++; break; }
+      }
+      if (deferred && cur_valid && chunk.size() == 1 && chunk[0].certain) {
+        set_slot_eval(0, chunk[0].op, chunk[0].q, hk[chunk[0].q]);
+        enqueue_replicas(1);
+        commit_eval(chunk[0].op, chunk[0].q, hk[chunk[0].q], 0);
+        err_pending = true;
+        *deferred = true;
+        n_deferred++;
+        *fwin = err;  // placeholder until resolve_err()
+        return chunk[0].ev;
       }
       if (!chunk.empty()) {
         for (size_t c = 0; c < chunk.size(); c++) set_slot_eval((int)c, chunk[c].op, chunk[c].q, hk[chunk[c].q]);
@@ -899,14 +981,9 @@ struct Session : SessionBase {
   void commit_eval(int op, int q, int k, int slot) {
     const T* a;
     const T* b;
-    if (slot >= 0) {
-      adopt_slot(slot);
-      a = slots[slot].ap;
-      b = slots[slot].bp;
-    } else {
-      a = eval_a(op, q);
-      b = eval_b(op, q);
-    }
+    if (slot >= 0) adopt_slot(slot);
+    a = eval_a(op, q);
+    b = eval_b(op, q);
     CK(cudaMemcpyAsync(Ut.p + (size_t)k * m, a, sizeof(T) * m, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(V.p + (size_t)k * n, b, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
     sync_factor_copies(k);
@@ -944,7 +1021,14 @@ struct Session : SessionBase {
     if (slot >= 0) ph[slot] += t - ph_t;
     ph_t = t;
   }
+  bool dhist_on = getenv("STMF_DHIST") != nullptr;
+  int64_t dhist[14] = {0};
   void ph_report() {
+    if (dhist_on) {
+      fprintf(stderr, "[stmf replica D log2 histogram]");
+      for (int b = 0; b < 14; b++) fprintf(stderr, " %lld", (long long)dhist[b]);
+      fprintf(stderr, "\n");
+    }
     if (phase_timing)
       fprintf(stderr, "[stmf phases ms] caches %.1f candidates %.1f eval %.1f decide %.1f\n", ph[0] * 1e3,
               ph[1] * 1e3, ph[2] * 1e3, ph[3] * 1e3);
@@ -977,7 +1061,8 @@ struct Session : SessionBase {
       ph_mark(2);
       R.evaluated += 2 * (int64_t)E;
       double f;
-      int w = decide_batch(E, hk, &f);
+      bool deferred = false;
+      int w = decide_batch(E, hk, &f, defer_accepts ? &deferred : nullptr);
       ph_mark(3);
       if (w >= 0) {
         R.attempts += w + 1;
@@ -985,9 +1070,14 @@ struct Session : SessionBase {
           row_depth[i] = t0 + w / 2 + 1;
           depth_ema = depth_ema > 0 ? 0.9 * depth_ema + 0.1 * (double)row_depth[i] : (double)row_depth[i];
         }
-        err = f;
         R.accepts++;
-        traj_append(R, run_now(R), err);
+        if (deferred) {
+          traj_append(R, run_now(R), std::nan(""));
+          pend_te = &R.te[R.len - 1];
+        } else {
+          err = f;
+          traj_append(R, run_now(R), err);
+        }
         return;
       }
       R.attempts += 2 * (int64_t)E;
@@ -1006,6 +1096,7 @@ struct Session : SessionBase {
   }
   int batch_floor = 1;
   bool fixed_sched = false;
+  bool defer_accepts = getenv("STMF_NO_DEFER") == nullptr;
 
   void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
            int64_t* counts) override {
@@ -1032,10 +1123,12 @@ struct Session : SessionBase {
           row_visit(R, i);
         }
         sweeps++;
+        resolve_err();
         traj_append(R, run_now(R), err);  // mark_sweep_boundary (engine.py:309-310)
         if (err_before - err < eps) break;
       }
     }
+    resolve_err();
     counts[0] = R.len; counts[1] = R.attempts; counts[2] = R.accepts; counts[3] = sweeps;
     ph_report();
     counts[4] = R.visits; counts[5] = R.evaluated; counts[6] = n_escalations - esc0;
@@ -1086,6 +1179,7 @@ struct Session : SessionBase {
     auto it = std::lower_bound(cols.begin(), cols.end(), (int32_t)j);
     if (it == cols.end() || *it != (int32_t)j) fail(STMF_ERR_INVALID, "entry (%lld, %lld) is missing", (long long)i, (long long)j);
     int64_t p = beg + (it - cols.begin());
+    resolve_err();
     if (!err_valid) objective();
     int32_t jj = (int32_t)j, kk = k;
     CK(cudaMemcpyAsync(cj.p, &jj, sizeof(int32_t), cudaMemcpyHostToDevice, st));

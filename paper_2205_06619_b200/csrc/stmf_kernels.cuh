@@ -16,6 +16,7 @@
 // to numpy (T = double) or to the binary32 restatement (T = float).
 #pragma once
 #include <cuda_runtime.h>
+#include <cub/block/block_merge_sort.cuh>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -560,7 +561,7 @@ struct Ilv {
 };
 
 template <typename T>
-__device__ __forceinline__ int64_t ilv_index(int q, int64_t a, int64_t len) {
+__host__ __device__ __forceinline__ int64_t ilv_index(int q, int64_t a, int64_t len) {
   constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
   int g = q / kEG, p = (q % kEG) / EGP, e = q % EGP;
   return (((int64_t)g * P + p) * len + a) * EGP + e;
@@ -985,16 +986,16 @@ __global__ void k_objective(int64_t m, const int64_t* __restrict__ ptr, const in
 template <typename T>
 __global__ void k_residuals(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                             const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
-                            const uint8_t* __restrict__ ag, int k, const T* __restrict__ a, const T* __restrict__ b,
-                            u64* __restrict__ out) {
+                            const uint8_t* __restrict__ ag, int k, const T* __restrict__ a, int as,
+                            const T* __restrict__ b, int bs, u64* __restrict__ out) {
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = w; r < m; r += nw) {
-    T ar = a[r];
+    T ar = a[r * as];
     for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
       T Q = (ag[p] == k) ? t2[p] : t1[p];
-      T pm = vmax(Q, add_rn(ar, b[idx[p]]));
+      T pm = vmax(Q, add_rn(ar, b[(int64_t)idx[p] * bs]));
       out[p] = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
     }
   }
@@ -1247,9 +1248,12 @@ __global__ void k_merge_delta(int64_t N, const u64* __restrict__ S_cur, const u6
 }
 
 // ---- the same replica steps for a round of slots in one launch each (slot = blockIdx.y)
+// A slot's factor vectors are read with a stride: 1 for a contiguous vector, EGP for
+// one eval of a planar interleaved phase-A buffer (no de-interleave copy needed).
 template <typename T>
 struct RepSlot {
   int k;
+  int as, bs;        // element strides of a / b
   const T* a;
   const T* b;
   u64* res;
@@ -1258,89 +1262,182 @@ struct RepSlot {
   u64* news;
   int* dcount;
   double* pw;
+  double* out;       // the replica's value (root of the pairwise tree)
 };
 
+// entry-parallel over the CSR entries (rowof = row of each entry); changed entries
+// are appended (warp ballot + one atomic) to the slot's (olds, news)
 template <typename T>
-__global__ void k_residuals_delta_multi(int64_t m, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+__global__ void k_residuals_delta_multi(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ idx,
                                         const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
                                         const uint8_t* __restrict__ ag, const u64* __restrict__ res_cur,
                                         const RepSlot<T>* __restrict__ slots) {
   const RepSlot<T> S = slots[blockIdx.y];
   int lane = threadIdx.x & 31;
-  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = w; r < m; r += nw) {
-    T ar = S.a[r];
-    int64_t beg = ptr[r], end = ptr[r + 1];
-    for (int64_t base = beg; base < end; base += 32) {
-      int64_t p = base + lane;
-      bool ch = false;
-      u64 nb = 0, ob = 0;
-      if (p < end) {
-        T Q = (ag[p] == S.k) ? t2[p] : t1[p];
-        T pm = vmax(Q, add_rn(ar, S.b[idx[p]]));
-        nb = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
-        ob = res_cur[p];
-        S.res[p] = nb;
-        ch = nb != ob;
-      }
-      unsigned bal = __ballot_sync(0xffffffffu, ch);
-      if (bal) {
-        int slot = 0;
-        if (lane == 0) slot = atomicAdd(S.dcount, __popc(bal));
-        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(bal & ((1u << lane) - 1));
-        if (ch && slot < kDeltaCap) { S.olds[slot] = ob; S.news[slot] = nb; }
-      }
-    }
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool ch = false;
+  u64 nb = 0, ob = 0;
+  if (p < N) {
+    T Q = (ag[p] == S.k) ? t2[p] : t1[p];
+    T pm = vmax(Q, add_rn(S.a[(int64_t)rowof[p] * S.as], S.b[(int64_t)idx[p] * S.bs]));
+    nb = (u64)__double_as_longlong((double)vabs(sub_rn(xv[p], pm)));
+    ob = res_cur[p];
+    S.res[p] = nb;
+    ch = nb != ob;
+  }
+  unsigned bal = __ballot_sync(0xffffffffu, ch);
+  if (bal) {
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(S.dcount, __popc(bal));
+    slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(bal & ((1u << lane) - 1));
+    if (ch && slot < kDeltaCap) { S.olds[slot] = ob; S.news[slot] = nb; }
   }
 }
 
+// ascending block merge sort of the D <= kDeltaCap changed values (block 0: olds,
+// block 1: news); the tile size follows D (block-uniform branch)
+struct U64Less {
+  __device__ __forceinline__ bool operator()(u64 a, u64 b) const { return a < b; }
+};
+constexpr int kSortThreads = 1024;
+template <int ITEMS>
+__device__ __forceinline__ void block_sort_u64(u64* a, int D, void* tmp_raw) {
+  using Sort = cub::BlockMergeSort<u64, kSortThreads, ITEMS>;
+  auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(tmp_raw);
+  u64 key[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    int e = threadIdx.x * ITEMS + i;
+    key[i] = e < D ? a[e] : ~0ull;
+  }
+  Sort(tmp).Sort(key, U64Less(), D, ~0ull);
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    int e = threadIdx.x * ITEMS + i;
+    if (e < D) a[e] = key[i];
+  }
+}
 template <typename T>
-__global__ void __launch_bounds__(1024) k_sort_delta_multi(const RepSlot<T>* __restrict__ slots) {
+__global__ void __launch_bounds__(kSortThreads) k_sort_delta_multi(const RepSlot<T>* __restrict__ slots) {
+  static_assert(kDeltaCap == 4 * kSortThreads, "two sort configurations");
+  __shared__ union {
+    typename cub::BlockMergeSort<u64, kSortThreads, 1>::TempStorage t1;
+    typename cub::BlockMergeSort<u64, kSortThreads, 4>::TempStorage t4;
+  } tmp;
   const RepSlot<T> S = slots[blockIdx.y];
-  __shared__ u64 sh[kDeltaCap];
   u64* a = blockIdx.x == 0 ? S.olds : S.news;
   int D = *S.dcount;
   if (D > kDeltaCap || D < 2) return;
-  int P = 1;
-  while (P < D) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) sh[i] = i < D ? a[i] : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        int l = i ^ j;
-        if (l > i) {
-          u64 x = sh[i], y = sh[l];
-          bool up = (i & k) == 0;
-          if ((x > y) == up) { sh[i] = y; sh[l] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < D; i += blockDim.x) a[i] = sh[i];
+  if (D <= kSortThreads) block_sort_u64<1>(a, D, &tmp);
+  else block_sort_u64<4>(a, D, &tmp);
 }
 
+// warp-cooperative 32-ary searches over a sorted u64 array (all lanes return the
+// result): first index with a[i] >= x (lower) or a[i] > x (upper)
+template <bool UPPER>
+__device__ __forceinline__ int64_t warp_bound_u64(const u64* __restrict__ a, int64_t n, u64 x, int lane) {
+  int64_t lo = 0, hi = n;  // the answer lies in [lo, hi]
+  while (hi - lo > 32) {
+    int64_t step = (hi - lo + 31) / 32;
+    int64_t idx = lo + (int64_t)(lane + 1) * step - 1;
+    bool v = idx < hi;
+    bool below = v && (UPPER ? a[idx] <= x : a[idx] < x);
+    int c = __popc(__ballot_sync(0xffffffffu, below));
+    int nv = __popc(__ballot_sync(0xffffffffu, v));
+    int64_t nlo = lo + (int64_t)c * step;
+    if (c < nv) hi = lo + (int64_t)(c + 1) * step - 1;
+    lo = nlo;
+  }
+  int64_t idx = lo + lane;
+  bool below = idx < hi && (UPPER ? a[idx] <= x : a[idx] < x);
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+// count of a[0, n) below x (UPPER: <= x), fixed trip count for a block-uniform n
+template <bool UPPER>
+__device__ __forceinline__ int bsearch_count(const u64* a, int n, int top, u64 x) {
+  int pos = 0;
+  for (int st = top; st > 0; st >>= 1)
+    if (pos + st <= n && (UPPER ? a[pos + st - 1] <= x : a[pos + st - 1] < x)) pos += st;
+  return pos;
+}
+
+// S_new = (S_cur - olds) U news, one block per tile of S_cur.  Tile b covers the
+// values [x0_b, x0_(b+1)): the olds / news of that range are located once per block
+// (warp-parallel 32-ary searches) and staged in shared memory, so each element's
+// searches are short shared-memory searches; the block also places the news of
+// its range.
+constexpr int kMergeTile = 1024, kMergeEpt = kMergeTile / 256, kMergeWin = 1024;
 template <typename T>
-__global__ void k_merge_delta_multi(int64_t N, const u64* __restrict__ S_cur, const RepSlot<T>* __restrict__ slots) {
+__global__ void __launch_bounds__(256) k_merge_delta_multi(int64_t N, const u64* __restrict__ S_cur,
+                                                           const RepSlot<T>* __restrict__ slots) {
   const RepSlot<T> S = slots[blockIdx.y];
   int D = *S.dcount;
   if (D > kDeltaCap) return;
   const u64* __restrict__ olds = S.olds;
   const u64* __restrict__ news = S.news;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < N) {
-    u64 x = S_cur[t];
-    int64_t le_old = upper_bound_u64(olds, D, x);
-    int64_t lt_old = lower_bound_u64(olds, D, x);
+  int64_t ntiles = (N + kMergeTile - 1) / kMergeTile;
+  bool last = (int64_t)blockIdx.x == ntiles - 1;
+  int64_t t0 = (int64_t)blockIdx.x * kMergeTile;
+  int64_t t1 = last ? N : t0 + kMergeTile;
+  __shared__ int64_t win[5];
+  __shared__ u64 so[kMergeWin], sn[kMergeWin];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u64 x0 = S_cur[t0];
+  if (wid < 5) {
+    u64 xn = last ? 0 : S_cur[t1];
+    int64_t v = 0;
+    switch (wid) {
+      case 0: v = warp_bound_u64<false>(olds, D, x0, lane); break;
+      case 1: v = last ? D : warp_bound_u64<true>(olds, D, xn, lane); break;
+      case 2: v = blockIdx.x == 0 ? 0 : warp_bound_u64<false>(news, D, x0, lane); break;
+      case 3: v = last ? D : warp_bound_u64<false>(news, D, xn, lane); break;
+      default: v = warp_bound_u64<false>(S_cur, N, x0, lane);  // first copy of x0
+    }
+    if (lane == 0) win[wid] = v;
+  }
+  __syncthreads();
+  int o0 = (int)win[0], on = (int)(win[1] - win[0]), n0 = (int)win[2], nn = (int)(win[3] - win[2]);
+  const u64* wo = olds + o0;
+  const u64* wn = news + n0;
+  if (on <= kMergeWin && nn <= kMergeWin) {
+    for (int i = threadIdx.x; i < on; i += blockDim.x) so[i] = wo[i];
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) sn[i] = wn[i];
+    wo = so;
+    wn = sn;
+  }
+  __syncthreads();
+  int topo = on ? 1 << (31 - __clz(on)) : 0, topn = nn ? 1 << (31 - __clz(nn)) : 0;
+  u64 x[kMergeEpt];
+  int le[kMergeEpt], lt[kMergeEpt], ln[kMergeEpt];
+#pragma unroll
+  for (int i = 0; i < kMergeEpt; i++) {
+    int64_t t = t0 + threadIdx.x + i * 256;
+    x[i] = t < t1 ? S_cur[t] : ~0ull;
+  }
+#pragma unroll
+  for (int i = 0; i < kMergeEpt; i++) {
+    le[i] = bsearch_count<true>(wo, on, topo, x[i]);
+    lt[i] = bsearch_count<false>(wo, on, topo, x[i]);
+    ln[i] = bsearch_count<false>(wn, nn, topn, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kMergeEpt; i++) {
+    int64_t t = t0 + threadIdx.x + i * 256;
+    if (t >= t1) continue;
     bool kept = true;
-    if (le_old > lt_old) kept = (t - lower_bound_u64(S_cur, N, x)) >= le_old - lt_old;
-    if (kept) S.sorted[t - le_old + lower_bound_u64(news, D, x)] = x;
-  } else if (t < N + D) {
-    int64_t q = t - N;
-    u64 y = news[q];
-    S.sorted[q + upper_bound_u64(S_cur, N, y) - upper_bound_u64(olds, D, y)] = y;
+    // equal values: the first (le - lt) copies of x in S_cur are the removed ones
+    if (le[i] > lt[i]) {
+      int64_t first = x[i] == x0 ? win[4] : t0 + lower_bound_u64(S_cur + t0, t - t0, x[i]);
+      kept = (t - first) >= le[i] - lt[i];
+    }
+    if (kept) S.sorted[t - (o0 + le[i]) + n0 + ln[i]] = x[i];
+  }
+  // the news y of this tile (x0 <= y < x0_next): upper_bound(S_cur, y) lies in [t0, t1]
+  for (int q = threadIdx.x; q < nn; q += blockDim.x) {
+    u64 y = wn[q];
+    int64_t ub = t0 + upper_bound_u64(S_cur + t0, t1 - t0, y);
+    S.sorted[n0 + q + ub - (o0 + bsearch_count<true>(wo, on, topo, y))] = y;
   }
 }
 
@@ -1377,6 +1474,7 @@ __global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff
       for (int i = body; i < n; i++) res = __dadd_rn(res, a[i]);
     }
     S.pw[lnode[t]] = res;
+    if (lnode[t] == 0) *S.out = res;  // a single-leaf tree
   }
 }
 
@@ -1392,5 +1490,31 @@ __global__ void k_pw_combine_multi(int H, const int32_t* __restrict__ lvl_off, c
     }
     __syncthreads();
   }
+  if (threadIdx.x == 0) *slots[blockIdx.y].out = val[0];
+}
+
+// the same with the whole tree staged in shared memory: node values (nnodes doubles)
+// and the internal nodes in level order as {node, left, right} triples
+template <typename T>
+__global__ void __launch_bounds__(1024) k_pw_combine_multi_smem(int H, int nnodes, int nops,
+                                                                const int32_t* __restrict__ lvl_off,
+                                                                const int4* __restrict__ ops,
+                                                                const RepSlot<T>* __restrict__ slots) {
+  extern __shared__ double sval[];
+  int4* sops = reinterpret_cast<int4*>(sval + ((nnodes + 1) & ~1));
+  int* slvl = reinterpret_cast<int*>(sops + nops);
+  double* val = slots[blockIdx.y].pw;
+  for (int i = threadIdx.x; i < nnodes; i += blockDim.x) sval[i] = val[i];
+  for (int i = threadIdx.x; i < nops; i += blockDim.x) sops[i] = ops[i];
+  for (int i = threadIdx.x; i <= H; i += blockDim.x) slvl[i] = lvl_off[i];
+  __syncthreads();
+  for (int h = 0; h < H; h++) {
+    for (int t = slvl[h] + threadIdx.x; t < slvl[h + 1]; t += blockDim.x) {
+      int4 o = sops[t];
+      sval[o.x] = __dadd_rn(sval[o.y], sval[o.z]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *slots[blockIdx.y].out = sval[0];
 }
 }  // namespace stmf
