@@ -271,6 +271,8 @@ struct Session : SessionBase {
   DevBuf<u64> ckeys, ckeys2;
   DevBuf<int32_t> cvals, cperm, cj, ck;
   DevBuf<T> cx, xrow_dense;
+  DevBuf<T> cmi, sq;  // CM^(-i) per k for the visited row; s_q of the batch's F-ULF evals
+  bool inline_ulf = getenv("STMF_INLINE") ? atoi(getenv("STMF_INLINE")) != 0 : true;
   // batch scratch
   int Emax = 512;
   DevBuf<T> vbuf, ubufB, ubufA, vbufB, dtmpA, dtmpB;
@@ -374,6 +376,7 @@ struct Session : SessionBase {
     CK(cudaStreamSynchronize(st));
     N = h_row_ptr[m];
     if (N == 0) fail(STMF_ERR_INVALID, "empty matrix");
+    if (N >= (1ll << 31)) fail(STMF_ERR_INVALID, "more than 2^31 - 1 given entries per device");
     for (int64_t i = 0; i < m; i++) {
       int64_t c = h_row_ptr[i + 1] - h_row_ptr[i];
       if (c == 0) fail(STMF_ERR_INVALID, "row %lld has no given entries", (long long)i);
@@ -439,6 +442,7 @@ struct Session : SessionBase {
     rm1.alloc((size_t)rank * m); rm2.alloc((size_t)rank * m); rmarg.alloc((size_t)rank * m);
     ckeys.alloc(n); ckeys2.alloc(n); cvals.alloc(n); cperm.alloc(n);
     cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
+    cmi.alloc((size_t)rank * n); sq.alloc(n);
     vbuf.alloc((size_t)Emax * n); ubufB.alloc((size_t)Emax * m);
     ubufA.alloc((size_t)Emax * m); vbufB.alloc((size_t)Emax * n);
     dtmpA.alloc(m); dtmpB.alloc(n);
@@ -830,6 +834,14 @@ struct Session : SessionBase {
   // ---- candidates of row i ------------------------------------------------------
   int64_t build_candidates(int64_t i) {
     int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
+    if (nc <= 4 * kCandThreads && rank <= 256) {
+      auto kern = nc <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
+      kern<<<1, kCandThreads, 0, st>>>((int)nc, n, rank, col_idx.p + beg, xr.p + beg, agr.p + beg, score.p,
+                                       colhist.p, cj.p, ck.p, cx.p, xrow_dense.p);
+      LAUNCH_CK();
+      row_cmi(i);
+      return nc;
+    }
     k_cand_keys<<<nblk(nc, 256), 256, 0, st>>>(nc, col_idx.p + beg, score.p, ckeys.p, cvals.p);
     LAUNCH_CK();
     size_t bytes = cubtmp_bytes;
@@ -840,7 +852,14 @@ struct Session : SessionBase {
                                                              cperm.p, colhist.p, cj.p, ck.p, cx.p);
     LAUNCH_CK();
     dense_row(i);
+    row_cmi(i);
     return nc;
+  }
+
+  // CM^(-i) for the visited row (the statistics are current within a row visit)
+  void row_cmi(int64_t i) {
+    k_cmi<T><<<nblk((int64_t)rank * n, 256), 256, 0, st>>>(n, rank, i, cm1.p, cm2.p, cmarg.p, cmi.p);
+    LAUNCH_CK();
   }
 
   void dense_row(int64_t i) {
@@ -866,7 +885,7 @@ struct Session : SessionBase {
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     int64_t G8 = (int64_t)((E + kEG - 1) / kEG) * kEG;
     k_phaseA_ulf<T><<<nblk(G8 * n, 256), 256, 0, st>>>(n, E, i, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
-                                                        xrow_dense.p, vbuf.p, chg_ulf);
+                                                        xrow_dense.p, vbuf.p, chg_ulf, sq.p);
     LAUNCH_CK();
     k_phaseA_urf_fill<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bj, bk, rm1.p, rm2.p, rmarg.p, ubufA.p);
     LAUNCH_CK();
@@ -877,6 +896,11 @@ struct Session : SessionBase {
     int ng = (E + kEG - 1) / kEG;
     SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf,
                 0, long_thr, group_major};
+    if (inline_ulf) {
+      sa.inl_base = cmi.p;
+      sa.inl_xr = xrow_dense.p;
+      sa.inl_s = sq.p;
+    }
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
                 0, long_thr, group_major};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
@@ -1186,6 +1210,7 @@ struct Session : SessionBase {
     CK(cudaMemcpyAsync(ck.p, &kk, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(cx.p, xr.p + p, sizeof(T), cudaMemcpyDeviceToDevice, st));
     dense_row(i);
+    row_cmi(i);
     eval_batch(i, 0, 1);
     CK(cudaStreamSynchronize(st));
     double fv;

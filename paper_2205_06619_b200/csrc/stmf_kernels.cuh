@@ -24,6 +24,10 @@ namespace stmf {
 
 typedef unsigned long long u64;
 
+struct U64Less {
+  __device__ __forceinline__ bool operator()(u64 a, u64 b) const { return a < b; }
+};
+
 // ----------------------------------------------------------------------------
 // scalar helpers (explicit _rn intrinsics: no contraction, no fast-math)
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -533,6 +537,55 @@ __global__ void k_cand_build(int64_t nc, int rank, const int32_t* __restrict__ c
   }
 }
 
+// _ranked_row_candidates + TD_A votes + the dense copy of row i in ONE block for
+// rows with nc <= 4 * 1024 given entries: keys ~score bits (descending score) with
+// the entry index as value, stable block merge sort (equal scores keep ascending
+// column order, np.argsort(-scores[cols], kind="stable"), strategies.py:187).
+constexpr int kCandThreads = 1024;
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(kCandThreads)
+k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const T* __restrict__ xrow,
+           const uint8_t* __restrict__ agrow, const double* __restrict__ score, const int32_t* __restrict__ colhist,
+           int32_t* __restrict__ cj, int32_t* __restrict__ ck, T* __restrict__ cx, T* __restrict__ xrow_dense) {
+  using Sort = cub::BlockMergeSort<u64, kCandThreads, ITEMS, int>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ int32_t rowhist[256];
+  for (int l = threadIdx.x; l < rank; l += blockDim.x) rowhist[l] = 0;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) xrow_dense[c] = tinf<T>();
+  __syncthreads();
+  u64 key[ITEMS];
+  int val[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    int p = threadIdx.x * ITEMS + i;
+    if (p < nc) {
+      int c = cols[p];
+      key[i] = ~(u64)__double_as_longlong(score[c]);
+      atomicAdd(&rowhist[agrow[p]], 1);
+      xrow_dense[c] = xrow[p];
+    } else {
+      key[i] = ~0ull;
+    }
+    val[i] = p;
+  }
+  Sort(tmp).StableSort(key, val, U64Less(), nc, ~0ull);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; i++) {
+    int t = threadIdx.x * ITEMS + i;
+    if (t >= nc) continue;
+    int p = val[i];
+    int j = cols[p];
+    const int32_t* h = colhist + (int64_t)j * rank;
+    int k = 0, best = -1;
+    for (int l = 0; l < rank; l++) {  // _vote: argmax of bincount, lowest index on ties
+      int v = rowhist[l] + h[l];
+      if (v > best) { best = v; k = l; }
+    }
+    cj[t] = j; ck[t] = k; cx[t] = xrow[p];
+  }
+}
+
 template <typename T>
 __global__ void k_fill(int64_t len, T* __restrict__ a, T v) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -560,6 +613,23 @@ struct Ilv {
   static constexpr int P = kEG / EGP;
 };
 
+// one 16-byte plane slot of the interleaved layout
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+  typedef float4 type;
+  template <int N>
+  __device__ __forceinline__ static void unpack(float4 a, float (&v)[N], int o) {
+    v[o] = a.x; v[o + 1] = a.y; v[o + 2] = a.z; v[o + 3] = a.w;
+  }
+};
+template <> struct Vec16<double> {
+  typedef double2 type;
+  template <int N>
+  __device__ __forceinline__ static void unpack(double2 a, double (&v)[N], int o) {
+    v[o] = a.x; v[o + 1] = a.y;
+  }
+};
+
 template <typename T>
 __host__ __device__ __forceinline__ int64_t ilv_index(int q, int64_t a, int64_t len) {
   constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
@@ -583,7 +653,8 @@ template <typename T>
 __global__ void k_phaseA_ulf(int64_t n, int E, int64_t i, const int32_t* __restrict__ cj,
                              const int32_t* __restrict__ ck, const T* __restrict__ cx, const T* __restrict__ V,
                              const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
-                             const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg) {
+                             const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg,
+                             T* __restrict__ s_out = nullptr) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int G = (E + kEG - 1) / kEG;
   if (t >= (int64_t)G * kEG * n) return;
@@ -597,7 +668,16 @@ __global__ void k_phaseA_ulf(int64_t n, int E, int64_t i, const int32_t* __restr
   T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
   T v = vmin(cmx, sub_rn(xrow_dense[c], s));
   vI[t] = v;
+  if (s_out && c == 0) s_out[q] = s;
   if (v != V[kn + c]) chg[q] = 1;
+}
+
+// CM^(-i) for every k: the column minima of X - U.k without row i (top-2 statistics)
+template <typename T>
+__global__ void k_cmi(int64_t n, int rank, int64_t i, const T* __restrict__ cm1, const T* __restrict__ cm2,
+                      const int32_t* __restrict__ cmarg, T* __restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < (int64_t)rank * n) out[t] = (cmarg[t] == (int32_t)i) ? cm2[t] : cm1[t];
 }
 
 // F-URF evals q: u'_r = min(RM^(-j)_r, X_rj - s'_q), s'_q = X_ij - U_ik
@@ -681,6 +761,11 @@ struct SideB {
   int64_t long_thr;  // lines with more entries are processed block-per-line (k_phaseB_long)
   int group_major;   // item order: 1 = eval-group major (entry data L2-resident: vin block
                      // stays hot in L1), 0 = line major (entry data streamed once per batch)
+  // F-ULF side only (else null): per-k base CM^(-i) (rank x len_other), the dense
+  // seed row X_i. (len_other) and s_q per eval, to recompute vin inline
+  const T* inl_base = nullptr;
+  const T* inl_xr = nullptr;
+  const T* inl_s = nullptr;
 };
 
 template <int EG, typename V>
@@ -706,6 +791,167 @@ __device__ __forceinline__ void load_eg(const double* __restrict__ g, int64_t le
   }
 }
 
+// the kEG first-residuation values of entry column c for the evals of a group:
+// VM 0/1 read the planar phase-A buffer (plane pointers pl[]); VM 2 (F-ULF, one k
+// for the group) recomputes them from the shared per-k base and the dense seed row,
+// exactly as phase A does: v'_q,c = min(CM^(-i)_kc, X_ic - s_q)
+template <typename T, int VM>
+__device__ __forceinline__ void eval_vals(const T* __restrict__ xr_row, const T* __restrict__ base,
+                                          const typename Vec16<T>::type* const (&pl)[Ilv<T>::P], const T (&s)[kEG],
+                                          int c, T (&v)[kEG]) {
+  if (VM == 2) {
+    T b = base[c], xr = xr_row[c];
+#pragma unroll
+    for (int q = 0; q < kEG; q++) v[q] = vmin(b, sub_rn(xr, s[q]));
+  } else {
+#pragma unroll
+    for (int p = 0; p < Ilv<T>::P; p++) Vec16<T>::unpack(__ldg(pl[p] + c), v, p * Ilv<T>::EGP);
+  }
+}
+
+// min / sum of kEG per-lane values over the warp with a transposed butterfly:
+// 4 + 2 + 1 exchanges halve the values per lane, then 2 plain steps.  Lane l ends
+// with the reduction of eval (l >> 2) & 7.
+template <typename V, bool SUM>
+__device__ __forceinline__ V warp_reduce8(const V (&v)[kEG], int lane) {
+  static_assert(kEG == 8, "transposed reduction of 8 evals");
+  auto op = [](V a, V b) -> V {
+    if constexpr (SUM) return __dadd_rn(a, b);
+    else return vmin(a, b);
+  };
+  bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  V t4[4], t2[2];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    V send = b4 ? v[j] : v[j + 4], keep = b4 ? v[j + 4] : v[j];
+    t4[j] = op(keep, shfl_xor(send, 16));
+  }
+#pragma unroll
+  for (int j = 0; j < 2; j++) {
+    V send = b3 ? t4[j] : t4[j + 2], keep = b3 ? t4[j + 2] : t4[j];
+    t2[j] = op(keep, shfl_xor(send, 8));
+  }
+  V r = op(b2 ? t2[1] : t2[0], shfl_xor(b2 ? t2[0] : t2[1], 4));
+  r = op(r, shfl_xor(r, 2));
+  return op(r, shfl_xor(r, 1));
+}
+
+// VM: 0 = planar, per-eval k; 1 = planar, one k for the group (Q shared per
+// entry); 2 = one k, F-ULF values recomputed inline (no per-eval gathers).
+// Entry offsets are 32-bit (N < 2^31 is checked at session creation).
+template <typename T, int UNR, int VM>
+__device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g, int e0, int ne,
+                                            const int (&kq)[kEG], int lane, int* __restrict__ flags, int F,
+                                            double exact_limit) {
+  constexpr int EG = kEG, P = Ilv<T>::P;
+  using V16 = typename Vec16<T>::type;
+  int64_t nlines = S.nlines;
+  const V16* pl[P];
+#pragma unroll
+  for (int p = 0; p < P; p++)
+    pl[p] = reinterpret_cast<const V16*>(S.vin) + ((int64_t)g * P + p) * S.len_other;
+  T s[EG];
+  const T* base = nullptr;
+  if (VM == 2) {
+    base = S.inl_base + (int64_t)kq[0] * S.len_other;
+#pragma unroll
+    for (int q = 0; q < EG; q++) s[q] = S.inl_s[e0 + (q < ne ? q : ne - 1)];
+  }
+  const int beg = (int)S.ptr[L], end = (int)S.ptr[L + 1];
+  const T* __restrict__ xv = S.xv;
+  const int32_t* __restrict__ idx = S.idx;
+  T mn[EG];
+  if (S.mode == 2) {
+    // sharded F-URF second half: the line values are the all-reduced minima
+#pragma unroll
+    for (int q = 0; q < EG; q++) mn[q] = S.out[(int64_t)(e0 + (q < ne ? q : ne - 1)) * nlines + L];
+  } else {
+#pragma unroll
+    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
+    // U entries per lane per iteration: their idx -> vin gathers are in flight
+    // together (the loop is latency-bound otherwise); missing slots use x = +inf
+    constexpr int U = sizeof(T) == 8 ? 2 : 4;  // pass 1 is cheap in registers: always unrolled
+    for (int p0 = beg + lane; p0 < end; p0 += 32 * U) {
+      T x[U];
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        int p = p0 + 32 * u;
+        bool ok = p < end;
+        x[u] = ok ? xv[p] : tinf<T>();
+        c[u] = ok ? idx[p] : 0;
+      }
+      T v[U][EG];
+#pragma unroll
+      for (int u = 0; u < U; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x[u], v[u][q]));
+    }
+    T r = warp_reduce8<T, false>(mn, lane);
+#pragma unroll
+    for (int q = 0; q < EG; q++) mn[q] = __shfl_sync(0xffffffffu, r, q << 2);
+  }
+  if (lane < ne) {
+    T w = lane_pick<EG>(mn, lane);
+    int kl = lane_pick<EG>(kq, lane);
+    if (S.mode != 2) S.out[(int64_t)(e0 + lane) * nlines + L] = w;
+    if (S.mode != 1 && w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
+  }
+  if (S.mode == 1) return;  // sharded F-URF first half: local minima only
+  double part[EG];
+#pragma unroll
+  for (int q = 0; q < EG; q++) part[q] = 0.0;
+  // |x - max(Q, w)| == |min(x - Q, x - w)| exactly (x - . is monotone under rounding)
+  constexpr int U2 = UNR;
+  for (int p0 = beg + lane; p0 < end; p0 += 32 * U2) {
+    T x[U2], a1[U2], a2[U2];
+    int a[U2], c[U2];
+#pragma unroll
+    for (int u = 0; u < U2; u++) {
+      int p = p0 + 32 * u;
+      bool ok = p < end;
+      int pp = ok ? p : beg;
+      x[u] = xv[pp];
+      c[u] = idx[pp];
+      a1[u] = S.t1[pp];
+      a2[u] = S.t2[pp];
+      a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the line (contributes 0)
+    }
+    T v[U2][EG];
+#pragma unroll
+    for (int u = 0; u < U2; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
+#pragma unroll
+    for (int u = 0; u < U2; u++) {
+      if (a[u] < 0) continue;
+      if (VM >= 1) {
+        T r1 = sub_rn(x[u], (a[u] == kq[0]) ? a2[u] : a1[u]);
+#pragma unroll
+        for (int q = 0; q < EG; q++)
+          part[q] = __dadd_rn(part[q], (double)vabs(vmin(r1, sub_rn(x[u], add_rn(mn[q], v[u][q])))));
+      } else {
+#pragma unroll
+        for (int q = 0; q < EG; q++) {
+          T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
+          T pm = vmax(Q, add_rn(mn[q], v[u][q]));
+          part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
+        }
+      }
+    }
+  }
+  double pv = warp_reduce8<double, true>(part, lane);
+  int q = (lane >> 2) & 7;
+  if ((lane & 3) == 0 && q < ne) {
+    int fl = 0;
+    if (!(pv < exact_limit)) fl |= 4;
+    u64 hi, lo;
+    fx_from_double(pv, F, hi, lo, fl);
+    fx_atomic_add(S.acc + 2 * (e0 + q), hi, lo);
+    if (fl & 6) atomicOr(flags, fl);
+  }
+}
+
 template <typename T, int UNR>
 __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E, const int32_t* __restrict__ ek,
                                             int lane, int* __restrict__ flags, int F, double exact_limit) {
@@ -726,96 +972,17 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   }
   int e0 = g * EG;
   int ne = E - e0 < EG ? E - e0 : EG;
-  const T* __restrict__ vg = S.vin + (int64_t)g * S.len_other * EG;
+  if (S.ptr[L + 1] - S.ptr[L] > S.long_thr) return;  // a long line: k_phaseB_long
   int kq[EG];
+  bool unif = true;
 #pragma unroll
-  for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
-  int64_t beg = S.ptr[L], end = S.ptr[L + 1];
-  if (end - beg > S.long_thr) return;  // a long line: k_phaseB_long
-  T mn[EG];
-  if (S.mode == 2) {
-    // sharded F-URF second half: the line values are the all-reduced minima
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = S.out[(int64_t)(e0 + (q < ne ? q : ne - 1)) * nlines + L];
-  } else {
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-    // U entries per lane per iteration: their idx -> vin gathers are in flight
-    // together (the loop is latency-bound otherwise); missing slots use x = +inf
-    constexpr int U = sizeof(T) == 8 ? 2 : 4;  // pass 1 is cheap in registers: always unrolled
-    for (int64_t p0 = beg + lane; p0 < end; p0 += 32 * U) {
-      T x[U];
-      int c[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        int64_t p = p0 + 32 * u;
-        bool ok = p < end;
-        x[u] = ok ? S.xv[p] : tinf<T>();
-        c[u] = ok ? S.idx[p] : 0;
-      }
-      T v[U][EG];
-#pragma unroll
-      for (int u = 0; u < U; u++) load_eg(vg, S.len_other, (int64_t)c[u], v[u]);
-#pragma unroll
-      for (int u = 0; u < U; u++)
-#pragma unroll
-        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x[u], v[u][q]));
-    }
-#pragma unroll
-    for (int q = 0; q < EG; q++)
-      for (int o = 16; o; o >>= 1) mn[q] = vmin(mn[q], shfl_xor(mn[q], o));
+  for (int q = 0; q < EG; q++) {
+    kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
+    unif &= kq[q] == kq[0];
   }
-  if (lane < ne) {
-    T w = lane_pick<EG>(mn, lane);
-    int kl = lane_pick<EG>(kq, lane);
-    if (S.mode != 2) S.out[(int64_t)(e0 + lane) * nlines + L] = w;
-    if (S.mode != 1 && w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
-  }
-  if (S.mode == 1) return;  // sharded F-URF first half: local minima only
-  double part[EG];
-#pragma unroll
-  for (int q = 0; q < EG; q++) part[q] = 0.0;
-  constexpr int U2 = UNR;
-  for (int64_t p0 = beg + lane; p0 < end; p0 += 32 * U2) {
-    T x[U2], a1[U2], a2[U2];
-    int a[U2], c[U2];
-#pragma unroll
-    for (int u = 0; u < U2; u++) {
-      int64_t p = p0 + 32 * u;
-      bool ok = p < end;
-      int64_t pp = ok ? p : beg;
-      x[u] = S.xv[pp];
-      c[u] = S.idx[pp];
-      a1[u] = S.t1[pp];
-      a2[u] = S.t2[pp];
-      a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the line (contributes 0)
-    }
-    T v[U2][EG];
-#pragma unroll
-    for (int u = 0; u < U2; u++) load_eg(vg, S.len_other, (int64_t)c[u], v[u]);
-#pragma unroll
-    for (int u = 0; u < U2; u++) {
-      if (a[u] < 0) continue;
-#pragma unroll
-      for (int q = 0; q < EG; q++) {
-        T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
-        T pm = vmax(Q, add_rn(mn[q], v[u][q]));
-        part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < EG; q++)
-    for (int o = 16; o; o >>= 1) part[q] = __dadd_rn(part[q], shfl_xor(part[q], o));
-  if (lane < ne) {
-    double pv = lane_pick<EG>(part, lane);
-    int fl = 0;
-    if (!(pv < exact_limit)) fl |= 4;
-    u64 hi, lo;
-    fx_from_double(pv, F, hi, lo, fl);
-    fx_atomic_add(S.acc + 2 * (e0 + lane), hi, lo);
-    if (fl & 6) atomicOr(flags, fl);
-  }
+  if (!unif) phaseB_body<T, UNR, 0>(S, L, g, e0, ne, kq, lane, flags, F, exact_limit);
+  else if (S.inl_base) phaseB_body<T, UNR, 2>(S, L, g, e0, ne, kq, lane, flags, F, exact_limit);
+  else phaseB_body<T, UNR, 1>(S, L, g, e0, ne, kq, lane, flags, F, exact_limit);
 }
 
 // Phase B of both update rules in one launch: items [0, A) are F-ULF evals on CSR
@@ -1296,9 +1463,6 @@ __global__ void k_residuals_delta_multi(int64_t N, const int32_t* __restrict__ r
 
 // ascending block merge sort of the D <= kDeltaCap changed values (block 0: olds,
 // block 1: news); the tile size follows D (block-uniform branch)
-struct U64Less {
-  __device__ __forceinline__ bool operator()(u64 a, u64 b) const { return a < b; }
-};
 constexpr int kSortThreads = 1024;
 template <int ITEMS>
 __device__ __forceinline__ void block_sort_u64(u64* a, int D, void* tmp_raw) {

@@ -439,6 +439,7 @@ struct ShardGroup : SessionBase {
     CK(cudaMemcpyAsync(s.h_row_ptr.data(), s.row_ptr.p, sizeof(int64_t) * (ml + 1), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     s.Nl = s.h_row_ptr[ml];
+    if (s.Nl >= (1ll << 31)) fail(STMF_ERR_INVALID, "more than 2^31 - 1 given entries per shard");
     for (int64_t i = 0; i < ml; i++) {
       int64_t c = s.h_row_ptr[i + 1] - s.h_row_ptr[i];
       if (c != row_nnz[s.r0 + i]) fail(STMF_ERR_INVALID, "row %lld: given count mismatch", (long long)(s.r0 + i));
