@@ -202,12 +202,22 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool own = true;
   void alloc(size_t cnt) {
-    if (p) { cudaFree(p); p = nullptr; }
+    if (p && own) cudaFree(p);
+    p = nullptr;
+    own = true;
     n = cnt;
     if (cnt) CK(cudaMalloc(&p, cnt * sizeof(T)));
   }
-  ~DevBuf() { if (p) cudaFree(p); }
+  // a non-owning view into another allocation
+  void view(T* ptr, size_t cnt) {
+    if (p && own) cudaFree(p);
+    p = ptr;
+    n = cnt;
+    own = false;
+  }
+  ~DevBuf() { if (p && own) cudaFree(p); }
 };
 
 template <typename T>
@@ -280,6 +290,8 @@ struct Session : SessionBase {
   DevBuf<int> chg, flags, findpos;
   u64* h_acc = nullptr;
   int* h_chg = nullptr;
+  DevBuf<u64> bstate;
+  u64* h_bstate = nullptr;
   int* h_flags = nullptr;
   // replica
   DevBuf<u64> res_cur, S_cur;
@@ -325,11 +337,10 @@ struct Session : SessionBase {
   ~Session() override {
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
-    if (h_acc) cudaFreeHost(h_acc);
+    if (h_bstate) cudaFreeHost(h_bstate);
     if (h_dcount) cudaFreeHost(h_dcount);
-    if (h_rep) cudaFreeHost(h_rep);
+    if (h_out) cudaFreeHost(h_out);
     if (h_pwv) cudaFreeHost(h_pwv);
-    if (h_chg) cudaFreeHost(h_chg);
     if (h_flags) cudaFreeHost(h_flags);
     if (st) cudaStreamDestroy(st);
   }
@@ -446,9 +457,16 @@ struct Session : SessionBase {
     vbuf.alloc((size_t)Emax * n); ubufB.alloc((size_t)Emax * m);
     ubufA.alloc((size_t)Emax * m); vbufB.alloc((size_t)Emax * n);
     dtmpA.alloc(m); dtmpB.alloc(n);
-    acc.alloc(4 * (size_t)Emax); chg.alloc(2 * (size_t)Emax); flags.alloc(4); findpos.alloc(2);
-    CK(cudaMallocHost(&h_acc, sizeof(u64) * 4 * Emax));
-    CK(cudaMallocHost(&h_chg, sizeof(int) * 2 * Emax));
+    // batch results in one block, [flags: 4 int][acc: 4E u64][chg: 2E int][hk: E int],
+    // zeroed with one memset and read back with one copy per batch
+    bstate.alloc(2 + 4 * (size_t)Emax + 2 * (size_t)Emax);
+    flags.view(reinterpret_cast<int*>(bstate.p), 4);
+    acc.view(bstate.p + 2, 4 * (size_t)Emax);
+    chg.view(reinterpret_cast<int*>(bstate.p + 2 + 4 * (size_t)Emax), 2 * (size_t)Emax);
+    findpos.alloc(2);
+    CK(cudaMallocHost(&h_bstate, sizeof(u64) * bstate.n));
+    h_acc = h_bstate + 2;
+    h_chg = reinterpret_cast<int*>(h_bstate + 2 + 4 * (size_t)Emax);
     CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
     h_flags[0] = h_flags[1] = 0;
     size_t b1 = 0, b2 = 0;
@@ -639,16 +657,22 @@ struct Session : SessionBase {
   std::vector<Slot> slots;
   int* h_dcount = nullptr;
   double* h_pwv = nullptr;
-  RepSlot<T>* h_rep = nullptr;
-  DevBuf<RepSlot<T>> d_rep;
+  double* h_out = nullptr;  // per slot: value, change count (bits)
   DevBuf<int> d_dcounts;
   DevBuf<double> d_pwout;
+  void unpack_out(int count) {
+    for (int i = 0; i < count; i++) {
+      h_pwv[i] = h_out[2 * i];
+      h_dcount[i] = (int)reinterpret_cast<const long long*>(h_out)[2 * i + 1];
+    }
+  }
 
   void alloc_slots() {
-    CK(cudaMallocHost(&h_rep, sizeof(RepSlot<T>) * kSlots));
-    d_rep.alloc(kSlots);
+    static_assert(kSlots == kRepSlots, "replica round size");
+    CK(cudaMallocHost(&h_out, sizeof(double) * 2 * kSlots));
     d_dcounts.alloc(kSlots);
-    d_pwout.alloc(kSlots);
+    CK(cudaMemset(d_dcounts.p, 0, sizeof(int) * kSlots));
+    d_pwout.alloc(2 * kSlots);
     slots.resize(kSlots);
     for (auto& s : slots) {
       s.res.alloc(N); s.sorted.alloc(N); s.olds.alloc(kDeltaCap); s.news.alloc(kDeltaCap); s.dcount.alloc(1);
@@ -691,6 +715,7 @@ struct Session : SessionBase {
       CK(cudaMemcpyAsync(h_pwv + i, s.pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
+    if (delta) unpack_out(count);
     bool redo = false;
     for (int i = 0; i < count; i++) {
       if (dhist_on) dhist[std::min(13, 32 - __builtin_clz((unsigned)h_dcount[i] | 1))]++;
@@ -714,24 +739,23 @@ struct Session : SessionBase {
     n_escalations += count;
     if (delta) {
       // one launch per step for the whole round (slot = blockIdx.y)
+      RepRound<T> rr{};
       for (int i = 0; i < count; i++) {
         Slot& s = slots[i];
-        h_rep[i] = RepSlot<T>{s.k, s.as, s.bs, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p,
-                              d_dcounts.p + i, s.pw.p, d_pwout.p + i};
+        rr.s[i] = RepSlot<T>{s.k, s.as, s.bs, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p,
+                             d_dcounts.p + i, s.pw.p, d_pwout.p + 2 * i};
       }
-      CK(cudaMemcpyAsync(d_rep.p, h_rep, sizeof(RepSlot<T>) * count, cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(d_dcounts.p, 0, sizeof(int) * count, st));
       k_residuals_delta_multi<T><<<dim3(nblk(N, 256), count), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p,
-                                                                              t2r.p, agr.p, res_cur.p, d_rep.p);
+                                                                              t2r.p, agr.p, res_cur.p, rr);
       LAUNCH_CK();
-      k_sort_delta_multi<T><<<dim3(2, count), kSortThreads, 0, st>>>(d_rep.p);
+      k_sort_delta_multi<T><<<dim3(2, count), kSortThreads, 0, st>>>(rr);
       LAUNCH_CK();
       unsigned mt = (unsigned)((N + kMergeTile - 1) / kMergeTile);
-      k_merge_delta_multi<T><<<dim3(mt, count), 256, 0, st>>>(N, S_cur.p, d_rep.p);
+      k_merge_delta_multi<T><<<dim3(mt, count), 256, 0, st>>>(N, S_cur.p, rr);
       LAUNCH_CK();
       int nl = (int)pw.loff.size();
       k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), count), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
-                                                                                     pw_lnode.p, d_rep.p);
+                                                                                     pw_lnode.p, rr);
       LAUNCH_CK();
       if (pw.H > 0) {
         int nops = (int)pw.lvl_nodes.size();
@@ -739,14 +763,13 @@ struct Session : SessionBase {
                     sizeof(int) * (size_t)(pw.H + 1);
         if (sm <= kCombineSmem)
           k_pw_combine_multi_smem<T><<<dim3(1, count), 1024, sm, st>>>(pw.H, pw.nnodes, nops, pw_lvloff.p, pw_ops.p,
-                                                                       d_rep.p);
+                                                                       rr);
         else
           k_pw_combine_multi<T><<<dim3(1, count), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
-                                                                  pw_right.p, d_rep.p);
+                                                                  pw_right.p, rr);
         LAUNCH_CK();
       }
-      CK(cudaMemcpyAsync(h_dcount, d_dcounts.p, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(h_pwv, d_pwout.p, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_out, d_pwout.p, sizeof(double) * 2 * count, cudaMemcpyDeviceToHost, st));
     }
   }
 
@@ -761,6 +784,7 @@ struct Session : SessionBase {
   void resolve_err() {
     if (!err_pending) return;
     CK(cudaStreamSynchronize(st));
+    unpack_out(1);
     double fr = h_pwv[0];
     if (h_dcount[0] > kDeltaCap) {
       // too many changed entries for the delta merge: sort the adopted residuals
@@ -872,26 +896,25 @@ struct Session : SessionBase {
 
   // ---- one speculative batch: candidates cj/ck/cx[t0, t0+E) of row i ------------
   void eval_batch(int64_t i, int64_t t0, int E, int* hk = nullptr) {
-    if (hk) CK(cudaMemcpyAsync(hk, ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
     const int32_t* bj = cj.p + t0;
     const int32_t* bk = ck.p + t0;
     const T* bx = cx.p + t0;
-    u64* acc_ulf = acc.p;
-    u64* acc_urf = acc.p + 2 * (size_t)E;
-    int* chg_ulf = chg.p;
-    int* chg_urf = chg.p + E;
-    CK(cudaMemsetAsync(acc.p, 0, sizeof(u64) * 4 * E, st));
-    CK(cudaMemsetAsync(chg.p, 0, sizeof(int) * 2 * E, st));
-    CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+    // per-batch layout of bstate: [flags: 4 int][acc: 4E u64][chg: 2E int][hk: E int]
+    u64* acc_ulf = bstate.p + 2;
+    u64* acc_urf = acc_ulf + 2 * (size_t)E;
+    int* chg_ulf = reinterpret_cast<int*>(acc_ulf + 4 * (size_t)E);
+    int* chg_urf = chg_ulf + E;
+    int* hk_dev = chg_ulf + 2 * E;
+    size_t zero_bytes = 16 + sizeof(u64) * 4 * E + sizeof(int) * 2 * E;
+    CK(cudaMemsetAsync(bstate.p, 0, zero_bytes, st));
     int64_t G8 = (int64_t)((E + kEG - 1) / kEG) * kEG;
-    k_phaseA_ulf<T><<<nblk(G8 * n, 256), 256, 0, st>>>(n, E, i, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
-                                                        xrow_dense.p, vbuf.p, chg_ulf, sq.p);
+    unsigned nb_ulf = nblk(G8 * n, 256), nb_urf = nblk(G8 * m, 256);
+    k_phaseA<T><<<nb_ulf + nb_urf, 256, 0, st>>>(m, n, E, i, nb_ulf, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
+                                                 xrow_dense.p, vbuf.p, chg_ulf, sq.p, rm1.p, rm2.p, rmarg.p, ubufA.p,
+                                                 hk_dev);
     LAUNCH_CK();
-    k_phaseA_urf_fill<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bj, bk, rm1.p, rm2.p, rmarg.p, ubufA.p);
-    LAUNCH_CK();
-    k_phaseA_urf_seed<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p);
-    LAUNCH_CK();
-    k_chk_ilv<T><<<nblk(G8 * m, 256), 256, 0, st>>>(m, E, bk, ubufA.p, Ut.p, chg_urf);
+    k_phaseA_urf_seed_chk<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p,
+                                                chg_urf);
     LAUNCH_CK();
     int ng = (E + kEG - 1) / kEG;
     SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf,
@@ -909,9 +932,14 @@ struct Session : SessionBase {
     LAUNCH_CK();
     if (profiling) CK(cudaEventRecord(ev_b1, st));
     phaseB_launches++;
-    CK(cudaMemcpyAsync(h_acc, acc.p, sizeof(u64) * 4 * E, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_chg, chg.p, sizeof(int) * 2 * E, cudaMemcpyDeviceToHost, st));
-    check_flags();
+    CK(cudaMemcpyAsync(h_bstate, bstate.p, zero_bytes + sizeof(int) * E, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h_acc = h_bstate + 2;
+    h_chg = reinterpret_cast<int*>(h_acc + 4 * (size_t)E);
+    if (hk) std::memcpy(hk, h_chg + 2 * E, sizeof(int) * E);
+    int fl = reinterpret_cast<const int*>(h_bstate)[0];
+    if (fl & ~1 & 7) fail(STMF_ERR_NUMERIC, "exact objective window violated (flags %d, grid 2^-%d)", fl, F);
+    if (kExact && (fl & 1)) fail(STMF_ERR_NUMERIC, "inexact fixed-point conversion in exact mode");
     if (profiling) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev_b0, ev_b1));

@@ -697,6 +697,71 @@ __global__ void k_phaseA_urf_fill(int64_t m, int E, const int32_t* __restrict__ 
   uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
 }
 
+// Both first residuations of a batch in one launch: blocks [0, nb_ulf) run the F-ULF
+// values (k_phaseA_ulf), the rest the F-URF fill (k_phaseA_urf_fill); block 0 also
+// copies the batch's factor indices next to the results the host reads back.
+template <typename T>
+__global__ void k_phaseA(int64_t m, int64_t n, int E, int64_t i, unsigned nb_ulf, const int32_t* __restrict__ cj,
+                         const int32_t* __restrict__ ck, const T* __restrict__ cx, const T* __restrict__ V,
+                         const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
+                         const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg_ulf,
+                         T* __restrict__ s_out, const T* __restrict__ rm1, const T* __restrict__ rm2,
+                         const int32_t* __restrict__ rmarg, T* __restrict__ uI, int* __restrict__ hk_out) {
+  int G = (E + kEG - 1) / kEG;
+  if (blockIdx.x < nb_ulf) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0)
+      for (int q = threadIdx.x; q < E; q += blockDim.x) hk_out[q] = ck[q];
+    if (t >= (int64_t)G * kEG * n) return;
+    int q;
+    int64_t c;
+    ilv_decode<T>(t, n, q, c);
+    if (q >= E) { vI[t] = tinf<T>(); return; }
+    int k = ck[q];
+    int64_t kn = (int64_t)k * n;
+    T s = sub_rn(cx[q], V[kn + cj[q]]);
+    T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
+    T v = vmin(cmx, sub_rn(xrow_dense[c], s));
+    vI[t] = v;
+    if (c == 0) s_out[q] = s;
+    if (v != V[kn + c]) chg_ulf[q] = 1;
+  } else {
+    int64_t t = (blockIdx.x - nb_ulf) * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)G * kEG * m) return;
+    int q;
+    int64_t r;
+    ilv_decode<T>(t, m, q, r);
+    if (q >= E) { uI[t] = tinf<T>(); return; }
+    int64_t km = (int64_t)ck[q] * m;
+    uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+  }
+}
+
+// F-URF seed column j of eval q = blockIdx.x (rows of column j), then the change
+// flag of the eval's whole first-residuation vector against the current U.k
+template <typename T>
+__global__ void k_phaseA_urf_seed_chk(int64_t m, int E, int64_t i, const int32_t* __restrict__ cj,
+                                      const int32_t* __restrict__ ck, const T* __restrict__ cx,
+                                      const T* __restrict__ Ut, const int64_t* __restrict__ col_ptr,
+                                      const int32_t* __restrict__ row_idx, const T* __restrict__ xc,
+                                      T* __restrict__ uI, int* __restrict__ chg_urf) {
+  int q = blockIdx.x;
+  if (q >= E) return;
+  int j = cj[q];
+  int64_t km = (int64_t)ck[q] * m;
+  T s = sub_rn(cx[q], Ut[km + i]);
+  T* u = uI + ilv_index<T>(q, 0, m);
+  constexpr int EGP = Ilv<T>::EGP;
+  for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
+    int64_t r = row_idx[p] * EGP;
+    u[r] = vmin(u[r], sub_rn(xc[p], s));
+  }
+  __syncthreads();
+  int ch = 0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) ch |= u[r * EGP] != Ut[km + r];
+  if (__syncthreads_or(ch) && threadIdx.x == 0) chg_urf[q] = 1;
+}
+
 template <typename T>
 __global__ void k_phaseA_urf_seed(int64_t m, int E, int64_t i, const int32_t* __restrict__ cj,
                                   const int32_t* __restrict__ ck, const T* __restrict__ cx,
@@ -1429,8 +1494,22 @@ struct RepSlot {
   u64* news;
   int* dcount;
   double* pw;
-  double* out;       // the replica's value (root of the pairwise tree)
+  double* out;       // [0] the replica's value (root of the pairwise tree), [1] bits: D
 };
+
+// one replica round's slots, passed by value (no descriptor upload per round)
+constexpr int kRepSlots = 8;
+template <typename T>
+struct RepRound {
+  RepSlot<T> s[kRepSlots];
+};
+
+// the round's outputs: value and change count, then the count is reset for the next round
+__device__ __forceinline__ void rep_finish(const double* root, int* dcount, double* out) {
+  out[0] = *root;
+  reinterpret_cast<long long*>(out)[1] = *dcount;
+  *dcount = 0;
+}
 
 // entry-parallel over the CSR entries (rowof = row of each entry); changed entries
 // are appended (warp ballot + one atomic) to the slot's (olds, news)
@@ -1438,8 +1517,8 @@ template <typename T>
 __global__ void k_residuals_delta_multi(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ idx,
                                         const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
                                         const uint8_t* __restrict__ ag, const u64* __restrict__ res_cur,
-                                        const RepSlot<T>* __restrict__ slots) {
-  const RepSlot<T> S = slots[blockIdx.y];
+                                        const RepRound<T> R) {
+  const RepSlot<T>& S = R.s[blockIdx.y];
   int lane = threadIdx.x & 31;
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool ch = false;
@@ -1482,13 +1561,13 @@ __device__ __forceinline__ void block_sort_u64(u64* a, int D, void* tmp_raw) {
   }
 }
 template <typename T>
-__global__ void __launch_bounds__(kSortThreads) k_sort_delta_multi(const RepSlot<T>* __restrict__ slots) {
+__global__ void __launch_bounds__(kSortThreads) k_sort_delta_multi(const RepRound<T> R) {
   static_assert(kDeltaCap == 4 * kSortThreads, "two sort configurations");
   __shared__ union {
     typename cub::BlockMergeSort<u64, kSortThreads, 1>::TempStorage t1;
     typename cub::BlockMergeSort<u64, kSortThreads, 4>::TempStorage t4;
   } tmp;
-  const RepSlot<T> S = slots[blockIdx.y];
+  const RepSlot<T>& S = R.s[blockIdx.y];
   u64* a = blockIdx.x == 0 ? S.olds : S.news;
   int D = *S.dcount;
   if (D > kDeltaCap || D < 2) return;
@@ -1534,8 +1613,8 @@ __device__ __forceinline__ int bsearch_count(const u64* a, int n, int top, u64 x
 constexpr int kMergeTile = 1024, kMergeEpt = kMergeTile / 256, kMergeWin = 1024;
 template <typename T>
 __global__ void __launch_bounds__(256) k_merge_delta_multi(int64_t N, const u64* __restrict__ S_cur,
-                                                           const RepSlot<T>* __restrict__ slots) {
-  const RepSlot<T> S = slots[blockIdx.y];
+                                                           const RepRound<T> R) {
+  const RepSlot<T>& S = R.s[blockIdx.y];
   int D = *S.dcount;
   if (D > kDeltaCap) return;
   const u64* __restrict__ olds = S.olds;
@@ -1607,8 +1686,8 @@ __global__ void __launch_bounds__(256) k_merge_delta_multi(int64_t N, const u64*
 
 template <typename T>
 __global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff, const int32_t* __restrict__ llen,
-                                   const int32_t* __restrict__ lnode, const RepSlot<T>* __restrict__ slots) {
-  const RepSlot<T> S = slots[blockIdx.y];
+                                   const int32_t* __restrict__ lnode, const RepRound<T> R) {
+  const RepSlot<T>& S = R.s[blockIdx.y];
   int lane = threadIdx.x & 31;
   int j = lane & 7;
   int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3);
@@ -1638,15 +1717,16 @@ __global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff
       for (int i = body; i < n; i++) res = __dadd_rn(res, a[i]);
     }
     S.pw[lnode[t]] = res;
-    if (lnode[t] == 0) *S.out = res;  // a single-leaf tree
+    if (lnode[t] == 0) rep_finish(S.pw, S.dcount, S.out);  // a single-leaf tree
   }
 }
 
 template <typename T>
 __global__ void k_pw_combine_multi(int H, const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ nodes,
                                    const int32_t* __restrict__ left, const int32_t* __restrict__ right,
-                                   const RepSlot<T>* __restrict__ slots) {
-  double* val = slots[blockIdx.y].pw;
+                                   const RepRound<T> R) {
+  const RepSlot<T>& S = R.s[blockIdx.y];
+  double* val = S.pw;
   for (int h = 0; h < H; h++) {
     for (int t = lvl_off[h] + threadIdx.x; t < lvl_off[h + 1]; t += blockDim.x) {
       int nd = nodes[t];
@@ -1654,7 +1734,7 @@ __global__ void k_pw_combine_multi(int H, const int32_t* __restrict__ lvl_off, c
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *slots[blockIdx.y].out = val[0];
+  if (threadIdx.x == 0) rep_finish(val, S.dcount, S.out);
 }
 
 // the same with the whole tree staged in shared memory: node values (nnodes doubles)
@@ -1663,11 +1743,12 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_pw_combine_multi_smem(int H, int nnodes, int nops,
                                                                 const int32_t* __restrict__ lvl_off,
                                                                 const int4* __restrict__ ops,
-                                                                const RepSlot<T>* __restrict__ slots) {
+                                                                const RepRound<T> R) {
   extern __shared__ double sval[];
   int4* sops = reinterpret_cast<int4*>(sval + ((nnodes + 1) & ~1));
   int* slvl = reinterpret_cast<int*>(sops + nops);
-  double* val = slots[blockIdx.y].pw;
+  const RepSlot<T>& S = R.s[blockIdx.y];
+  double* val = S.pw;
   for (int i = threadIdx.x; i < nnodes; i += blockDim.x) sval[i] = val[i];
   for (int i = threadIdx.x; i < nops; i += blockDim.x) sops[i] = ops[i];
   for (int i = threadIdx.x; i <= H; i += blockDim.x) slvl[i] = lvl_off[i];
@@ -1679,6 +1760,6 @@ __global__ void __launch_bounds__(1024) k_pw_combine_multi_smem(int H, int nnode
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *slots[blockIdx.y].out = sval[0];
+  if (threadIdx.x == 0) rep_finish(sval, S.dcount, S.out);
 }
 }  // namespace stmf
