@@ -269,23 +269,32 @@ def run_b200(args):
     value = args.steps * world / t_dev_max
     gentries = attempts_all * N / t_dev_max / 1e9
 
-    # roofline of the dominant kernel (phase B): algorithmic bytes per launch =
-    # one pass over the given entries in each of its two orders (CSR rows for F-ULF,
-    # CSC columns for F-URF): 2 * (N * s + ceil(m*n/8)) (values + bitmask)
+    # roofline of the dominant kernel (phase B).  SURVEY.md §8(d): one attempt (a
+    # candidate evaluation over all N given entries) needs B_attempt = 2 * B_pass
+    # algorithmic bytes, B_pass = N*s + ceil(m*n/8) (values + bitmask); one launch
+    # evaluates every candidate of its batch (both rules), so its algorithmic bytes
+    # are B_attempt * (evaluations in the launch).  Launch times: CUDA events on the
+    # session stream around every phase-B launch (stmf_set_profiling).
     s_bytes = work.dtype.itemsize
-    b_launch = 2 * (N * s_bytes + (m * n + 7) // 8)
+    b_pass = N * s_bytes + (m * n + 7) // 8
     nb = c1["phaseB_timed"] - c0["phaseB_timed"]
     b_ns = c1["phaseB_ns"] - c0["phaseB_ns"]
     avg_s = b_ns / 1e9 / max(nb, 1)
+    evals_per_launch = evaluated / max(nb, 1)
+    b_launch = 2 * b_pass * evals_per_launch
     peak, peak_src = peaks()
     achieved = b_launch / avg_s / 1e9 if nb else None
+    l2_resident = 2 * N * (3 * s_bytes + 5) < 0.5 * 126e6
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": None,
                 "kernel": "stmf::k_phaseB (candidate evaluation: 2nd residuation + error, both rules)",
-                "bytes_per_launch": b_launch, "avg_launch_us": avg_s * 1e6, "launches": nb,
+                "bytes_per_launch": b_launch, "bytes_per_attempt": 2 * b_pass,
+                "evals_per_launch": evals_per_launch, "avg_launch_us": avg_s * 1e6, "launches": nb,
                 "share_of_step": (b_ns / 1e9) / t_dev if t_dev else None, "peak_source": peak_src,
-                "note": "working set is L2-resident at this config: the kernel is bound by the fp64 "
-                        "pipe/issue rate, not HBM (DESIGN.md §roofline)"}
+                "note": ("one pass over the given entries serves a group of 8 evaluations and the working "
+                         "set is L2-resident, so the HBM-equivalent rate can exceed the HBM peak; the kernel "
+                         "is issue-bound on fp64 compare/select (DESIGN.md, profiles/)") if l2_resident else
+                        "one pass over the given entries serves a group of 8 evaluations (DESIGN.md)"}
 
     line = None
     if rank == 0:

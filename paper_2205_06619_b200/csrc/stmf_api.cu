@@ -384,7 +384,7 @@ struct Session : SessionBase {
     h_row_ptr.resize(m + 1); h_col_ptr.resize(n + 1);
     CK(cudaMemcpyAsync(h_row_ptr.data(), row_ptr.p, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_col_ptr.data(), col_ptr.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     N = h_row_ptr[m];
     if (N == 0) fail(STMF_ERR_INVALID, "empty matrix");
     if (N >= (1ll << 31)) fail(STMF_ERR_INVALID, "more than 2^31 - 1 given entries per device");
@@ -494,7 +494,7 @@ struct Session : SessionBase {
     cubtmp_bytes = std::max(b1, b2);
     cubtmp.alloc(cubtmp_bytes);
     stats_dirty.assign(rank, 1);
-    CK(cudaStreamSynchronize(st));
+    ssync();
   }
   int gridX = -1000;
 
@@ -541,7 +541,7 @@ struct Session : SessionBase {
         LAUNCH_CK();
       }
     }
-    CK(cudaStreamSynchronize(st));
+    ssync();
     sync_factor_copies(-1);
     have_factors = true;
     cur_valid = false;
@@ -556,7 +556,7 @@ struct Session : SessionBase {
     std::vector<T> ut((size_t)rank * m);
     CK(cudaMemcpyAsync(ut.data(), Ut.p, sizeof(T) * ut.size(), cudaMemcpyDeviceToHost, st));
     if (Vh) CK(cudaMemcpyAsync(Vh, V.p, sizeof(T) * (size_t)rank * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     if (Uh) {
       T* U = (T*)Uh;
       for (int64_t i = 0; i < m; i++)
@@ -570,7 +570,7 @@ struct Session : SessionBase {
 
   void check_flags() {
     CK(cudaMemcpyAsync(h_flags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     if (h_flags[0] & ~1 & 7) {
       int f = h_flags[0];
       fail(STMF_ERR_NUMERIC, "exact objective window violated (flags %d, grid 2^-%d)", f, F);
@@ -601,7 +601,7 @@ struct Session : SessionBase {
           col.alloc(m);
           k_colscore_single<T><<<1, 32, 0, st>>>(m, col_ptr.p, row_idx.p, xc.p, t1c.p, col.p, score.p);
           LAUNCH_CK();
-          CK(cudaStreamSynchronize(st));
+          ssync();
         }
       }
       n_product_passes++;
@@ -714,7 +714,7 @@ struct Session : SessionBase {
       pw_sum(s);
       CK(cudaMemcpyAsync(h_pwv + i, s.pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     }
-    CK(cudaStreamSynchronize(st));
+    ssync();
     if (delta) unpack_out(count);
     bool redo = false;
     for (int i = 0; i < count; i++) {
@@ -729,7 +729,7 @@ struct Session : SessionBase {
       CK(cudaMemcpyAsync(h_pwv + i, slots[i].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
       redo = true;
     }
-    if (redo) CK(cudaStreamSynchronize(st));
+    if (redo) ssync();
   }
 
   // the delta replica steps of slots[0, count) on the stream, results copied to
@@ -783,7 +783,7 @@ struct Session : SessionBase {
 
   void resolve_err() {
     if (!err_pending) return;
-    CK(cudaStreamSynchronize(st));
+    ssync();
     unpack_out(1);
     double fr = h_pwv[0];
     if (h_dcount[0] > kDeltaCap) {
@@ -800,7 +800,7 @@ struct Session : SessionBase {
         LAUNCH_CK();
       }
       CK(cudaMemcpyAsync(h_pwv, slots[0].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      ssync();
       fr = h_pwv[0];
     } else {
       n_delta_replicas++;
@@ -933,7 +933,7 @@ struct Session : SessionBase {
     if (profiling) CK(cudaEventRecord(ev_b1, st));
     phaseB_launches++;
     CK(cudaMemcpyAsync(h_bstate, bstate.p, zero_bytes + sizeof(int) * E, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     h_acc = h_bstate + 2;
     h_chg = reinterpret_cast<int*>(h_acc + 4 * (size_t)E);
     if (hk) std::memcpy(hk, h_chg + 2 * E, sizeof(int) * E);
@@ -1068,14 +1068,30 @@ struct Session : SessionBase {
   double ph_t = 0;
   void ph_mark(int slot) {
     if (!phase_timing) return;
-    CK(cudaStreamSynchronize(st));
+    ssync();
     double t = now_s();
     if (slot >= 0) ph[slot] += t - ph_t;
     ph_t = t;
   }
+  // host time spent waiting for the stream (STMF_SYNC_STATS): the rest of the run's
+  // wall time is host work during which the GPU may idle
+  bool sync_stats = getenv("STMF_SYNC_STATS") != nullptr;
+  double t_wait = 0;
+  int64_t n_sync = 0;
+  void ssync() {
+    if (!sync_stats) {
+      CK(cudaStreamSynchronize(st));
+      return;
+    }
+    double t = now_s();
+    CK(cudaStreamSynchronize(st));
+    t_wait += now_s() - t;
+    n_sync++;
+  }
   bool dhist_on = getenv("STMF_DHIST") != nullptr;
   int64_t dhist[14] = {0};
   void ph_report() {
+    if (sync_stats) fprintf(stderr, "[stmf sync] %lld syncs, %.1f ms waiting\n", (long long)n_sync, t_wait * 1e3);
     if (dhist_on) {
       fprintf(stderr, "[stmf replica D log2 histogram]");
       for (int b = 0; b < 14; b++) fprintf(stderr, " %lld", (long long)dhist[b]);
@@ -1194,7 +1210,7 @@ struct Session : SessionBase {
     if (P) CK(cudaMemcpyAsync(P, t1r.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
     if (top2) CK(cudaMemcpyAsync(top2, t2r.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(a.data(), agr.p, N, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     if (arg)
       for (int64_t p = 0; p < N; p++) arg[p] = a[p];
   }
@@ -1202,7 +1218,7 @@ struct Session : SessionBase {
   void col_scores(double* out) override {
     ensure_caches();
     CK(cudaMemcpyAsync(out, score.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
   }
 
   void residuate(int axis, const void* vec, void* out) override {
@@ -1216,7 +1232,7 @@ struct Session : SessionBase {
       k_line_min<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, dv.p, dout.p);
     LAUNCH_CK();
     CK(cudaMemcpyAsync(out, dout.p, sizeof(T) * lout, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
   }
 
   void try_update(int op, int64_t i, int64_t j, int k, void* ucol, void* vrow, double* f, bool commit_if_better,
@@ -1227,7 +1243,7 @@ struct Session : SessionBase {
     int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
     std::vector<int32_t> cols(nc);
     CK(cudaMemcpyAsync(cols.data(), col_idx.p + beg, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     auto it = std::lower_bound(cols.begin(), cols.end(), (int32_t)j);
     if (it == cols.end() || *it != (int32_t)j) fail(STMF_ERR_INVALID, "entry (%lld, %lld) is missing", (long long)i, (long long)j);
     int64_t p = beg + (it - cols.begin());
@@ -1240,7 +1256,7 @@ struct Session : SessionBase {
     dense_row(i);
     row_cmi(i);
     eval_batch(i, 0, 1);
-    CK(cudaStreamSynchronize(st));
+    ssync();
     double fv;
     if (!h_chg[op]) {
       fv = err;
@@ -1253,7 +1269,7 @@ struct Session : SessionBase {
     }
     if (ucol) CK(cudaMemcpyAsync(ucol, eval_a(op, 0), sizeof(T) * m, cudaMemcpyDeviceToHost, st));
     if (vrow) CK(cudaMemcpyAsync(vrow, eval_b(op, 0), sizeof(T) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     *f = fv;
     if (commit_if_better) {
       *accepted = fv < err;
@@ -1288,7 +1304,7 @@ struct Session : SessionBase {
     }
     LAUNCH_CK();
     CK(cudaMemcpyAsync(h_acc, acc.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    ssync();
     *ms = total / std::max(reps, 1);
     *errout = fx_to_double(h_acc[1], h_acc[0], F);
     dirty = true;  // the bench overwrote the CSR caches without second-argmax tracking
