@@ -27,6 +27,7 @@
 
 #include "stmf_b200.h"
 #include "stmf_kernels.cuh"
+#include "stmf_graph.cuh"
 
 using namespace stmf;
 
@@ -335,6 +336,8 @@ struct Session : SessionBase {
   std::vector<int> batch_sched;
 
   ~Session() override {
+    graph_destroy();
+    if (h_ctl) cudaFreeHost(h_ctl);
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
     if (h_bstate) cudaFreeHost(h_bstate);
@@ -740,6 +743,7 @@ struct Session : SessionBase {
     if (delta) {
       // one launch per step for the whole round (slot = blockIdx.y)
       RepRound<T> rr{};
+      rr.count = count;
       for (int i = 0; i < count; i++) {
         Slot& s = slots[i];
         rr.s[i] = RepSlot<T>{s.k, s.as, s.bs, s.ap, s.bp, s.res.p, s.sorted.p, s.olds.p, s.news.p,
@@ -823,6 +827,7 @@ struct Session : SessionBase {
   void adopt_slot(int s) {
     std::swap(res_cur.p, slots[s].res.p);
     std::swap(S_cur.p, slots[s].sorted.p);
+    ptr_epoch++;  // a captured sweep graph holds the old pointers
     cur_valid = true;
   }
 
@@ -861,9 +866,9 @@ struct Session : SessionBase {
     if (nc <= 4 * kCandThreads && rank <= 256) {
       auto kern = nc <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
       kern<<<1, kCandThreads, 0, st>>>((int)nc, n, rank, col_idx.p + beg, xr.p + beg, agr.p + beg, score.p,
-                                       colhist.p, cj.p, ck.p, cx.p, xrow_dense.p);
+                                       colhist.p, cj.p, ck.p, cx.p, xrow_dense.p, i, cm1.p, cm2.p, cmarg.p, cmi.p,
+                                       nullptr, nullptr);
       LAUNCH_CK();
-      row_cmi(i);
       return nc;
     }
     k_cand_keys<<<nblk(nc, 256), 256, 0, st>>>(nc, col_idx.p + beg, score.p, ckeys.p, cvals.p);
@@ -1155,6 +1160,15 @@ struct Session : SessionBase {
     if ((int64_t)row_depth.size() == m) row_depth[i] = nc;
   }
   std::vector<int64_t> row_depth;  // candidates consumed at each row's last visit
+  bool rdepth_on_dev = false;      // the device copy (graph sweeps) is the current one
+  void pull_row_depth() {
+    if (!rdepth_on_dev) return;
+    h_rdepth.resize(m);
+    CK(cudaMemcpyAsync(h_rdepth.data(), d_row_depth.p, sizeof(long long) * m, cudaMemcpyDeviceToHost, st));
+    ssync();
+    for (int64_t i = 0; i < m; i++) row_depth[i] = h_rdepth[i];
+    rdepth_on_dev = false;
+  }
   double depth_ema = 0;            // running mean of accepting depths
   // first batch = scale * previous depth + add; later batches grow by `growth`
   double sched_scale = 1.25, sched_growth = 2.0;
@@ -1165,6 +1179,286 @@ struct Session : SessionBase {
   int batch_floor = 1;
   bool fixed_sched = false;
   bool defer_accepts = getenv("STMF_NO_DEFER") == nullptr;
+
+  // ---- device-resident sweeps (stmf_graph.cuh) ----------------------------------------
+  // One CUDA graph per sweep: the host loop of run()/row_visit/decide_batch as nested
+  // conditional nodes.  Built lazily; rebuilt when buffers it captured were swapped.
+  bool graph_on = getenv("STMF_GRAPH") ? atoi(getenv("STMF_GRAPH")) != 0 : true;
+  int64_t ptr_epoch = 0, graph_epoch = -1;
+  bool graph_prof = false;
+  cudaGraph_t g_top = nullptr;
+  cudaGraphExec_t g_exec = nullptr;
+  DevBuf<DevCtl> dctl;
+  DevCtl* h_ctl = nullptr;
+  DevBuf<long long> d_row_depth;
+  DevBuf<double> d_traj_t, d_traj_e;
+  DevBuf<RepRound<T>> d_rr;
+  DevBuf<double*> d_pwptr;
+  DevBuf<double> d_aval;
+  std::vector<long long> h_rdepth;
+  std::vector<double> h_traj_t, h_traj_e;
+
+  bool graph_eligible() const {
+    // rows must fit the one-block candidate ranking; column scores of a single-column
+    // matrix and fixed batch schedules stay on the host loop
+    return graph_on && !fixed_sched && max_rownnz <= 4 * kCandThreads && rank <= 256 && n > 1 &&
+           (kExact || cur_valid) && n_long_rows + n_long_cols == 0 && 2 * Emax <= kDecideThreads;
+  }
+
+  void graph_destroy() {
+    if (g_exec) cudaGraphExecDestroy(g_exec);
+    if (g_top) cudaGraphDestroy(g_top);
+    g_exec = nullptr;
+    g_top = nullptr;
+  }
+
+  // capture helpers: kernels launched on st between cap_begin / cap_end are appended
+  // to graph g after deps; cap_end returns the new leaf nodes
+  void cap_begin(cudaGraph_t g, const std::vector<cudaGraphNode_t>& deps) {
+    CK(cudaStreamBeginCaptureToGraph(st, g, deps.empty() ? nullptr : deps.data(), nullptr, deps.size(),
+                                     cudaStreamCaptureModeThreadLocal));
+  }
+  std::vector<cudaGraphNode_t> cap_end(cudaGraph_t g) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg;
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+    std::vector<cudaGraphNode_t> out(deps, deps + nd);
+    CK(cudaStreamEndCapture(st, &g));
+    return out;
+  }
+  // a conditional node after deps; returns its body graph
+  cudaGraph_t add_cond(cudaGraph_t g, std::vector<cudaGraphNode_t>& deps, cudaGraphConditionalHandle h,
+                       cudaGraphConditionalNodeType type) {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps.empty() ? nullptr : deps.data(), deps.size(), &cp));
+    deps.assign(1, node);
+    return cp.conditional.phGraph_out[0];
+  }
+
+  GBufs<T> gbufs() {
+    GBufs<T> B{};
+    B.bst = bstate.p; B.ck = ck.p;
+    B.ubufB = ubufB.p; B.vbuf = vbuf.p; B.ubufA = ubufA.p; B.vbufB = vbufB.p;
+    B.m = m; B.n = n;
+    B.row_depth = d_row_depth.p;
+    B.traj_t = d_traj_t.p; B.traj_e = d_traj_e.p;
+    B.rr = d_rr.p;
+    for (int s = 0; s < kSlots && !kExact; s++) {
+      B.res[s] = slots[s].res.p; B.sorted[s] = slots[s].sorted.p;
+      B.olds[s] = slots[s].olds.p; B.news[s] = slots[s].news.p; B.pw[s] = slots[s].pw.p;
+    }
+    B.dcount = d_dcounts.p;
+    B.out = d_pwout.p;
+    B.F = F;
+    B.exact = kExact;
+    for (int op = 0; op < 2; op++) {
+      int64_t L = op == 0 ? (max_rownnz + 31) / 32 : (max_colnnz + 31) / 32;
+      B.dr[op] = (double)(L + 8) * std::ldexp(1.0, -53);
+      B.da[op] = (double)(op == 0 ? m : n) * std::ldexp(1.0, -F + 1);
+    }
+    B.beta = beta_rel;
+    B.aval = d_aval.p;
+    return B;
+  }
+
+  void graph_build() {
+    graph_destroy();
+    if (!dctl.p) {
+      dctl.alloc(1);
+      CK(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
+      d_row_depth.alloc(m);
+      d_traj_t.alloc(m + 1);
+      d_traj_e.alloc(m + 1);
+      d_rr.alloc(1);
+      d_pwptr.alloc(kSlots);
+      d_aval.alloc(2 * (size_t)Emax);
+      h_traj_t.resize(m + 1);
+      h_traj_e.resize(m + 1);
+    }
+    if (!kExact) {
+      std::vector<double*> pp(kSlots);
+      for (int s = 0; s < kSlots; s++) pp[s] = slots[s].pw.p;
+      CK(cudaMemcpy(d_pwptr.p, pp.data(), sizeof(double*) * kSlots, cudaMemcpyHostToDevice));
+    }
+    GBufs<T> B = gbufs();
+    DevCtl* c = dctl.p;
+    CK(cudaGraphCreate(&g_top, 0));
+    cudaGraphConditionalHandle h_row, h_batch, h_acc, h_esc = 0, h_fb = 0;
+    CK(cudaGraphConditionalHandleCreate(&h_row, g_top, 0, 0));
+    std::vector<cudaGraphNode_t> d0;
+    cap_begin(g_top, d0);
+    k_g_sweep_begin<<<1, 1, 0, st>>>(c, m, h_row);
+    d0 = cap_end(g_top);
+    cudaGraph_t b_row = add_cond(g_top, d0, h_row, cudaGraphCondTypeWhile);
+
+    // ---- row body
+    CK(cudaGraphConditionalHandleCreate(&h_batch, b_row, 0, 0));
+    CK(cudaGraphConditionalHandleCreate(&h_acc, b_row, 0, 0));
+    std::vector<cudaGraphNode_t> dr;
+    cap_begin(b_row, dr);
+    k_g_row_begin<<<1, 1, 0, st>>>(c, row_ptr.p, d_row_depth.p, h_batch, h_acc);
+    {
+      auto kern = max_rownnz <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
+      kern<<<1, kCandThreads, 0, st>>>(0, n, rank, col_idx.p, xr.p, agr.p, score.p, colhist.p, cj.p, ck.p, cx.p,
+                                       xrow_dense.p, 0, cm1.p, cm2.p, cmarg.p, cmi.p, c, row_ptr.p);
+    }
+    dr = cap_end(b_row);
+    cudaGraph_t b_batch = add_cond(b_row, dr, h_batch, cudaGraphCondTypeWhile);
+
+    // ---- batch body
+    if (!kExact) CK(cudaGraphConditionalHandleCreate(&h_esc, b_batch, 0, 0));
+    std::vector<cudaGraphNode_t> db;
+    cap_begin(b_batch, db);
+    k_g_zero<<<8, 256, 0, st>>>(c, bstate.p);
+    k_phaseA<T><<<(unsigned)nsm * 4, 256, 0, st>>>(m, n, 0, 0, 0, cj.p, ck.p, cx.p, V.p, cm1.p, cm2.p, cmarg.p,
+                                                   xrow_dense.p, vbuf.p, nullptr, sq.p, rm1.p, rm2.p, rmarg.p,
+                                                   ubufA.p, nullptr, c, bstate.p);
+    k_phaseA_urf_seed_chk<T><<<Emax, 128, 0, st>>>(m, 0, 0, cj.p, ck.p, cx.p, Ut.p, col_ptr.p, row_idx.p, xc.p,
+                                                    ubufA.p, nullptr, c, bstate.p);
+    if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c);
+    {
+      SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, nullptr, nullptr,
+                  0, long_thr, group_major};
+      if (inline_ulf) {
+        sa.inl_base = cmi.p;
+        sa.inl_xr = xrow_dense.p;
+        sa.inl_s = sq.p;
+      }
+      SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, nullptr, nullptr,
+                  0, long_thr, group_major};
+      unsigned gb = (unsigned)nsm * (sizeof(T) == 8 && unroll > 1 ? 2 : 3);
+      if (unroll >= 4) gb = (unsigned)nsm * 2;
+      if (unroll >= 4)
+        k_phaseB<T, 4><<<gb, 256, 0, st>>>(sa, sb, 0, nullptr, flags.p, F, exact_limit, c, bstate.p, ck.p);
+      else if (unroll == 2)
+        k_phaseB<T, 2><<<gb, 256, 0, st>>>(sa, sb, 0, nullptr, flags.p, F, exact_limit, c, bstate.p, ck.p);
+      else
+        k_phaseB<T, 1><<<gb, 256, 0, st>>>(sa, sb, 0, nullptr, flags.p, F, exact_limit, c, bstate.p, ck.p);
+    }
+    k_g_decide<T><<<1, kDecideThreads, 0, st>>>(c, B, h_batch, h_acc, h_esc);
+    db = cap_end(b_batch);
+    if (!kExact) {
+      cudaGraph_t b_esc = add_cond(b_batch, db, h_esc, cudaGraphCondTypeWhile);
+      CK(cudaGraphConditionalHandleCreate(&h_fb, b_esc, 0, 0));
+      std::vector<cudaGraphNode_t> de;
+      cap_begin(b_esc, de);
+      RepRound<T> none{};
+      RepRound<T>* rp_ = d_rr.p;
+      k_residuals_delta_multi<T><<<dim3(nblk(N, 256), kSlots), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p,
+                                                                              t2r.p, agr.p, res_cur.p, none, rp_);
+      k_sort_delta_multi<T><<<dim3(2, kSlots), kSortThreads, 0, st>>>(none, rp_);
+      unsigned mt = (unsigned)((N + kMergeTile - 1) / kMergeTile);
+      k_merge_delta_multi<T><<<dim3(mt, kSlots), 256, 0, st>>>(N, S_cur.p, none, rp_);
+      int nl = (int)pw.loff.size();
+      k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), kSlots), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
+                                                                                     pw_lnode.p, none, rp_);
+      if (pw.H > 0) {
+        int nops = (int)pw.lvl_nodes.size();
+        size_t sm = sizeof(double) * (size_t)((pw.nnodes + 1) & ~1) + sizeof(int4) * (size_t)nops +
+                    sizeof(int) * (size_t)(pw.H + 1);
+        if (sm <= kCombineSmem)
+          k_pw_combine_multi_smem<T><<<dim3(1, kSlots), 1024, sm, st>>>(pw.H, pw.nnodes, nops, pw_lvloff.p,
+                                                                        pw_ops.p, none, rp_);
+        else
+          k_pw_combine_multi<T><<<dim3(1, kSlots), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
+                                                                   pw_right.p, none, rp_);
+      }
+      k_g_fb_check<<<1, 1, 0, st>>>(c, d_pwout.p, h_fb);
+      de = cap_end(b_esc);
+      cudaGraph_t b_fb = add_cond(b_esc, de, h_fb, cudaGraphCondTypeIf);
+      {
+        std::vector<cudaGraphNode_t> df;
+        cap_begin(b_fb, df);
+        for (int s = 0; s < kSlots; s++) {
+          full_sort(slots[s]);
+          pw_sum(slots[s]);
+        }
+        k_g_fb_fix<<<1, 32, 0, st>>>(c, d_pwptr.p, d_pwout.p);
+        cap_end(b_fb);
+      }
+      cap_begin(b_esc, de);
+      k_g_decide_esc<T><<<1, kDecideThreads, 0, st>>>(c, B, h_batch, h_acc, h_esc);
+      cap_end(b_esc);
+    }
+
+    // ---- accept (after the batch loop)
+    cudaGraph_t b_acc = add_cond(b_row, dr, h_acc, cudaGraphCondTypeIf);
+    {
+      std::vector<cudaGraphNode_t> da;
+      cap_begin(b_acc, da);
+      unsigned gc = (unsigned)nsm * 4;
+      k_g_commit<T><<<gc, 256, 0, st>>>(c, B, Ut.p, V.p, Urm.p, Vcm.p, rp, N, kExact ? nullptr : res_cur.p,
+                                        kExact ? nullptr : S_cur.p);
+      unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
+      const int* kc = &c->cache_k;
+      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
+                                           t1r.p, t2r.p, agr.p, a2r.p, kc);
+      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
+                                           t1c.p, t2c.p, agc.p, a2c.p, kc);
+      k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
+                                                   !kExact, exact_limit, flags.p);
+      k_line_stats<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p, cm1.p, cm2.p, cmarg.p, 0,
+                                                        kc, m, n);
+      k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
+                                                        kc, n, m);
+      cap_end(b_acc);
+    }
+    cap_begin(b_row, dr);
+    k_g_row_end<<<1, 1, 0, st>>>(c, bstate.p, kExact, m, h_row);
+    cap_end(b_row);
+    CK(cudaGraphInstantiate(&g_exec, g_top, 0));
+    graph_epoch = ptr_epoch;
+  }
+
+  // one sweep as one graph launch; returns false if the graph path does not apply
+  void graph_sweep(RunState& R) {
+    if (!g_exec || graph_epoch != ptr_epoch || graph_prof != profiling) {
+      graph_prof = profiling;
+      graph_build();
+    }
+    DevCtl& h = *h_ctl;
+    std::memset(&h, 0, sizeof(DevCtl));
+    h.err = err;
+    h.traj_cap = m + 1;
+    h.sweep = (double)R.cur_sweep;
+    h.sched_scale = sched_scale; h.sched_growth = sched_growth; h.sched_add = sched_add;
+    h.batch_floor = batch_floor; h.Emax = Emax; h.first0 = batch_sched[0];
+    h.cache_k = -1;
+    h.tb0 = 0;
+    CK(cudaMemcpyAsync(dctl.p, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+    CK(cudaGraphLaunch(g_exec, st));
+    CK(cudaMemcpyAsync(h_ctl, dctl.p, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_traj_t.data(), d_traj_t.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_traj_e.data(), d_traj_e.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
+    ssync();
+    if (h.error == 1) fail(STMF_ERR_NUMERIC, "decision bound violated (device decision)");
+    if (h.error == 2) fail(STMF_ERR_CAPACITY, "device trajectory capacity exceeded");
+    if (h.error == 3) fail(STMF_ERR_NUMERIC, "exact objective window violated (graph sweep, grid 2^-%d)", F);
+    for (long long t = 0; t < h.traj_len; t++) traj_append(R, h_traj_t[t], h_traj_e[t]);
+    err = h.err;
+    R.attempts += h.attempts;
+    R.accepts += h.accepts;
+    R.visits += h.visits;
+    R.evaluated += h.evaluated;
+    n_escalations += h.escalations;
+    n_product_passes += h.accepts;
+    phaseB_launches += h.batches;
+    if (graph_prof) {
+      phaseB_ns += (long long)h.phaseB_ns;
+      phaseB_timed += h.batches;
+    }
+    // kernel nodes executed: row (3), batch (5 + tick), escalation round (7 + 1), accept (6)
+    g_launches += h.visits * 3 + h.batches * (5 + (graph_prof ? 1 : 0)) + h.esc_rounds * 8 + h.accepts * 6;
+    if (h.accepts) dirty = false;
+    cache_k = -1;
+  }
 
   void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
            int64_t* counts) override {
@@ -1186,9 +1480,21 @@ struct Session : SessionBase {
         if (out_of_time(R)) break;
         R.cur_sweep = sweeps + 1;
         double err_before = err;
-        for (int64_t i = 0; i < m; i++) {
-          if (out_of_time(R)) break;
-          row_visit(R, i);
+        if (!R.wall && graph_eligible()) {
+          if (!rdepth_on_dev) {
+            h_rdepth.assign(row_depth.begin(), row_depth.end());
+            if (!d_row_depth.p) d_row_depth.alloc(m);
+            CK(cudaMemcpyAsync(d_row_depth.p, h_rdepth.data(), sizeof(long long) * m, cudaMemcpyHostToDevice, st));
+            rdepth_on_dev = true;
+          }
+          ensure_caches();
+          graph_sweep(R);
+        } else {
+          pull_row_depth();
+          for (int64_t i = 0; i < m; i++) {
+            if (out_of_time(R)) break;
+            row_visit(R, i);
+          }
         }
         sweeps++;
         resolve_err();
@@ -1197,6 +1503,7 @@ struct Session : SessionBase {
       }
     }
     resolve_err();
+    pull_row_depth();
     counts[0] = R.len; counts[1] = R.attempts; counts[2] = R.accepts; counts[3] = sweeps;
     ph_report();
     counts[4] = R.visits; counts[5] = R.evaluated; counts[6] = n_escalations - esc0;

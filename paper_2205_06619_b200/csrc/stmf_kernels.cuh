@@ -28,6 +28,34 @@ struct U64Less {
   __device__ __forceinline__ bool operator()(u64 a, u64 b) const { return a < b; }
 };
 
+// Control state of the device-resident sweep (stmf_graph.cuh): the kernels of a
+// captured CUDA graph read their per-row / per-batch parameters from here.
+struct DevCtl {
+  int64_t i;             // row being visited
+  int64_t nc;            // its candidates
+  int64_t t0;            // first candidate of the current batch
+  int E, next;           // batch size, next batch size
+  int accepted;          // the row visit accepted an update
+  int win_op, win_q, win_k, win_slot;
+  int cache_k;           // factor index of the last commit
+  double err;            // current objective
+  // fp64 decision scan over the batch's 2E evals (reference order)
+  int pos, nchunk;
+  int ch_ev[8], ch_q[8], ch_op[8], ch_cert[8];
+  int fb[8];             // slot needs the full-sort fallback
+  // run bookkeeping
+  long long attempts, accepts, visits, evaluated, escalations, traj_len, traj_cap;
+  long long batches, esc_rounds;
+  unsigned long long tb0, phaseB_ns;  // graph-mode phase-B timing (%globaltimer)
+  double sweep;          // trajectory time stamp of this sweep
+  int error;             // 1: decision bound violated, 2: trajectory capacity
+  int stop;              // time budget reached
+  unsigned long long deadline_ns;  // %globaltimer deadline (0: none)
+  // schedule (Session::row_visit)
+  double sched_scale, sched_growth;
+  int sched_add, batch_floor, Emax, first0;
+};
+
 // ----------------------------------------------------------------------------
 // scalar helpers (explicit _rn intrinsics: no contraction, no fast-math)
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -353,7 +381,9 @@ template <typename T>
 __global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
                            int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
                            const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
-                           T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2) {
+                           T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2,
+                           const int* __restrict__ kdev = nullptr) {
+  if (kdev) k = *kdev;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
     {
       int64_t r = rowof[p], c = colof[p];
@@ -469,7 +499,15 @@ __device__ __forceinline__ Top2<T> top2_warp(Top2<T> t) {
 template <typename T>
 __global__ void k_line_stats(int64_t nlines, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                              const T* __restrict__ xv, const T* __restrict__ other, T* __restrict__ s1,
-                             T* __restrict__ s2, int32_t* __restrict__ sarg, int idx_offset = 0) {
+                             T* __restrict__ s2, int32_t* __restrict__ sarg, int idx_offset = 0,
+                             const int* __restrict__ kdev = nullptr, int64_t kso = 0, int64_t kss = 0) {
+  if (kdev) {  // graph mode: factor index from the control block (row/col strides kso / kss)
+    int k = *kdev;
+    other += k * kso;
+    s1 += k * kss;
+    s2 += k * kss;
+    sarg += k * kss;
+  }
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -546,12 +584,25 @@ template <typename T, int ITEMS>
 __global__ void __launch_bounds__(kCandThreads)
 k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const T* __restrict__ xrow,
            const uint8_t* __restrict__ agrow, const double* __restrict__ score, const int32_t* __restrict__ colhist,
-           int32_t* __restrict__ cj, int32_t* __restrict__ ck, T* __restrict__ cx, T* __restrict__ xrow_dense) {
+           int32_t* __restrict__ cj, int32_t* __restrict__ ck, T* __restrict__ cx, T* __restrict__ xrow_dense,
+           int64_t irow, const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
+           T* __restrict__ cmi, const DevCtl* __restrict__ g = nullptr, const int64_t* __restrict__ row_ptr = nullptr) {
   using Sort = cub::BlockMergeSort<u64, kCandThreads, ITEMS, int>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ int32_t rowhist[256];
+  if (g) {  // graph mode: the row from the control block
+    irow = g->i;
+    int64_t beg = row_ptr[irow];
+    nc = (int)(row_ptr[irow + 1] - beg);
+    cols += beg;
+    xrow += beg;
+    agrow += beg;
+  }
   for (int l = threadIdx.x; l < rank; l += blockDim.x) rowhist[l] = 0;
   for (int64_t c = threadIdx.x; c < n; c += blockDim.x) xrow_dense[c] = tinf<T>();
+  // CM^(-i) of every k for the visited row (k_cmi)
+  for (int64_t t = threadIdx.x; t < (int64_t)rank * n; t += blockDim.x)
+    cmi[t] = (cmarg[t] == (int32_t)irow) ? cm2[t] : cm1[t];
   __syncthreads();
   u64 key[ITEMS];
   int val[ITEMS];
@@ -706,34 +757,49 @@ __global__ void k_phaseA(int64_t m, int64_t n, int E, int64_t i, unsigned nb_ulf
                          const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
                          const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg_ulf,
                          T* __restrict__ s_out, const T* __restrict__ rm1, const T* __restrict__ rm2,
-                         const int32_t* __restrict__ rmarg, T* __restrict__ uI, int* __restrict__ hk_out) {
+                         const int32_t* __restrict__ rmarg, T* __restrict__ uI, int* __restrict__ hk_out,
+                         const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr) {
+  unsigned nb_total = gridDim.x;
+  if (g) {  // graph mode: batch window from the control block, grid-stride over virtual blocks
+    E = g->E;
+    i = g->i;
+    cj += g->t0;
+    ck += g->t0;
+    cx += g->t0;
+    chg_ulf = reinterpret_cast<int*>(bst + 2 + 4 * (int64_t)E);
+    int64_t G8 = (int64_t)((E + kEG - 1) / kEG) * kEG;
+    nb_ulf = (unsigned)((G8 * n + 255) / 256);
+    nb_total = nb_ulf + (unsigned)((G8 * m + 255) / 256);
+  }
   int G = (E + kEG - 1) / kEG;
-  if (blockIdx.x < nb_ulf) {
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (blockIdx.x == 0)
-      for (int q = threadIdx.x; q < E; q += blockDim.x) hk_out[q] = ck[q];
-    if (t >= (int64_t)G * kEG * n) return;
-    int q;
-    int64_t c;
-    ilv_decode<T>(t, n, q, c);
-    if (q >= E) { vI[t] = tinf<T>(); return; }
-    int k = ck[q];
-    int64_t kn = (int64_t)k * n;
-    T s = sub_rn(cx[q], V[kn + cj[q]]);
-    T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
-    T v = vmin(cmx, sub_rn(xrow_dense[c], s));
-    vI[t] = v;
-    if (c == 0) s_out[q] = s;
-    if (v != V[kn + c]) chg_ulf[q] = 1;
-  } else {
-    int64_t t = (blockIdx.x - nb_ulf) * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= (int64_t)G * kEG * m) return;
-    int q;
-    int64_t r;
-    ilv_decode<T>(t, m, q, r);
-    if (q >= E) { uI[t] = tinf<T>(); return; }
-    int64_t km = (int64_t)ck[q] * m;
-    uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+  for (unsigned vb = blockIdx.x; vb < nb_total; vb += gridDim.x) {
+    if (vb < nb_ulf) {
+      int64_t t = vb * (int64_t)blockDim.x + threadIdx.x;
+      if (vb == 0 && hk_out)
+        for (int q = threadIdx.x; q < E; q += blockDim.x) hk_out[q] = ck[q];
+      if (t >= (int64_t)G * kEG * n) continue;
+      int q;
+      int64_t c;
+      ilv_decode<T>(t, n, q, c);
+      if (q >= E) { vI[t] = tinf<T>(); continue; }
+      int k = ck[q];
+      int64_t kn = (int64_t)k * n;
+      T s = sub_rn(cx[q], V[kn + cj[q]]);
+      T cmx = (cmarg[kn + c] == (int32_t)i) ? cm2[kn + c] : cm1[kn + c];
+      T v = vmin(cmx, sub_rn(xrow_dense[c], s));
+      vI[t] = v;
+      if (c == 0) s_out[q] = s;
+      if (v != V[kn + c]) chg_ulf[q] = 1;
+    } else {
+      int64_t t = (vb - nb_ulf) * (int64_t)blockDim.x + threadIdx.x;
+      if (t >= (int64_t)G * kEG * m) continue;
+      int q;
+      int64_t r;
+      ilv_decode<T>(t, m, q, r);
+      if (q >= E) { uI[t] = tinf<T>(); continue; }
+      int64_t km = (int64_t)ck[q] * m;
+      uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+    }
   }
 }
 
@@ -744,7 +810,16 @@ __global__ void k_phaseA_urf_seed_chk(int64_t m, int E, int64_t i, const int32_t
                                       const int32_t* __restrict__ ck, const T* __restrict__ cx,
                                       const T* __restrict__ Ut, const int64_t* __restrict__ col_ptr,
                                       const int32_t* __restrict__ row_idx, const T* __restrict__ xc,
-                                      T* __restrict__ uI, int* __restrict__ chg_urf) {
+                                      T* __restrict__ uI, int* __restrict__ chg_urf,
+                                      const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr) {
+  if (g) {
+    E = g->E;
+    i = g->i;
+    cj += g->t0;
+    ck += g->t0;
+    cx += g->t0;
+    chg_urf = reinterpret_cast<int*>(bst + 2 + 4 * (int64_t)E) + E;
+  }
   int q = blockIdx.x;
   if (q >= E) return;
   int j = cj[q];
@@ -1050,13 +1125,29 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   else phaseB_body<T, UNR, 1>(S, L, g, e0, ne, kq, lane, flags, F, exact_limit);
 }
 
+// graph mode: the batch window and the result slots of bstate
+// ([flags: 4 int][acc: 4E u64][chg: 2E int]) from the control block
+template <typename T>
+__device__ __forceinline__ void batch_from_ctl(const DevCtl* g, u64* bst, SideB<T>& A, SideB<T>& B, int& E) {
+  E = g->E;
+  A.acc = bst + 2;
+  B.acc = bst + 2 + 2 * (int64_t)E;
+  A.chg = reinterpret_cast<int*>(bst + 2 + 4 * (int64_t)E);
+  B.chg = A.chg + E;
+}
+
 // Phase B of both update rules in one launch: items [0, A) are F-ULF evals on CSR
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
 // UNR = entries per lane per loop iteration (memory-level parallelism vs registers)
 template <typename T, int UNR>
 __global__ void __launch_bounds__(256, UNR > 2 ? 2 : (sizeof(T) == 8 && UNR > 1 ? 2 : 3))
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
-         double exact_limit) {
+         double exact_limit, const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr,
+         const int32_t* __restrict__ ck = nullptr) {
+  if (g) {
+    batch_from_ctl(g, bst, A, B, E);
+    ek = ck + g->t0;
+  }
   int lane = threadIdx.x & 31;
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1075,7 +1166,12 @@ k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __r
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_phaseB_long(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, const int32_t* __restrict__ longA,
-              int nA, const int32_t* __restrict__ longB, int nB, int* __restrict__ flags, int F, double exact_limit) {
+              int nA, const int32_t* __restrict__ longB, int nB, int* __restrict__ flags, int F, double exact_limit,
+              const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr, const int32_t* __restrict__ ck = nullptr) {
+  if (g) {
+    batch_from_ctl(g, bst, A, B, E);
+    ek = ck + g->t0;
+  }
   constexpr int EG = kEG;
   __shared__ T smn[8][EG];
   __shared__ double spart[8][EG];
@@ -1502,7 +1598,13 @@ constexpr int kRepSlots = 8;
 template <typename T>
 struct RepRound {
   RepSlot<T> s[kRepSlots];
+  int count;
 };
+// a kernel's slot: from the by-value round (host-driven) or, in graph mode, from
+// the round the device-side decision wrote (Rp); blocks past the round's count exit
+#define REP_SLOT(S)                                                   \
+  if ((int)blockIdx.y >= (Rp ? Rp->count : R.count)) return;          \
+  const RepSlot<T> S = Rp ? Rp->s[blockIdx.y] : R.s[blockIdx.y]
 
 // the round's outputs: value and change count, then the count is reset for the next round
 __device__ __forceinline__ void rep_finish(const double* root, int* dcount, double* out) {
@@ -1517,8 +1619,8 @@ template <typename T>
 __global__ void k_residuals_delta_multi(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ idx,
                                         const T* __restrict__ xv, const T* __restrict__ t1, const T* __restrict__ t2,
                                         const uint8_t* __restrict__ ag, const u64* __restrict__ res_cur,
-                                        const RepRound<T> R) {
-  const RepSlot<T>& S = R.s[blockIdx.y];
+                                        const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
+  REP_SLOT(S);
   int lane = threadIdx.x & 31;
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool ch = false;
@@ -1561,13 +1663,13 @@ __device__ __forceinline__ void block_sort_u64(u64* a, int D, void* tmp_raw) {
   }
 }
 template <typename T>
-__global__ void __launch_bounds__(kSortThreads) k_sort_delta_multi(const RepRound<T> R) {
+__global__ void __launch_bounds__(kSortThreads) k_sort_delta_multi(const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
   static_assert(kDeltaCap == 4 * kSortThreads, "two sort configurations");
   __shared__ union {
     typename cub::BlockMergeSort<u64, kSortThreads, 1>::TempStorage t1;
     typename cub::BlockMergeSort<u64, kSortThreads, 4>::TempStorage t4;
   } tmp;
-  const RepSlot<T>& S = R.s[blockIdx.y];
+  REP_SLOT(S);
   u64* a = blockIdx.x == 0 ? S.olds : S.news;
   int D = *S.dcount;
   if (D > kDeltaCap || D < 2) return;
@@ -1613,8 +1715,8 @@ __device__ __forceinline__ int bsearch_count(const u64* a, int n, int top, u64 x
 constexpr int kMergeTile = 1024, kMergeEpt = kMergeTile / 256, kMergeWin = 1024;
 template <typename T>
 __global__ void __launch_bounds__(256) k_merge_delta_multi(int64_t N, const u64* __restrict__ S_cur,
-                                                           const RepRound<T> R) {
-  const RepSlot<T>& S = R.s[blockIdx.y];
+                                                           const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
+  REP_SLOT(S);
   int D = *S.dcount;
   if (D > kDeltaCap) return;
   const u64* __restrict__ olds = S.olds;
@@ -1686,8 +1788,8 @@ __global__ void __launch_bounds__(256) k_merge_delta_multi(int64_t N, const u64*
 
 template <typename T>
 __global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff, const int32_t* __restrict__ llen,
-                                   const int32_t* __restrict__ lnode, const RepRound<T> R) {
-  const RepSlot<T>& S = R.s[blockIdx.y];
+                                   const int32_t* __restrict__ lnode, const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
+  REP_SLOT(S);
   int lane = threadIdx.x & 31;
   int j = lane & 7;
   int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3);
@@ -1724,8 +1826,8 @@ __global__ void k_pw_leaves8_multi(int nleaves, const int64_t* __restrict__ loff
 template <typename T>
 __global__ void k_pw_combine_multi(int H, const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ nodes,
                                    const int32_t* __restrict__ left, const int32_t* __restrict__ right,
-                                   const RepRound<T> R) {
-  const RepSlot<T>& S = R.s[blockIdx.y];
+                                   const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
+  REP_SLOT(S);
   double* val = S.pw;
   for (int h = 0; h < H; h++) {
     for (int t = lvl_off[h] + threadIdx.x; t < lvl_off[h + 1]; t += blockDim.x) {
@@ -1743,11 +1845,11 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_pw_combine_multi_smem(int H, int nnodes, int nops,
                                                                 const int32_t* __restrict__ lvl_off,
                                                                 const int4* __restrict__ ops,
-                                                                const RepRound<T> R) {
+                                                                const RepRound<T> R, const RepRound<T>* __restrict__ Rp = nullptr) {
   extern __shared__ double sval[];
   int4* sops = reinterpret_cast<int4*>(sval + ((nnodes + 1) & ~1));
   int* slvl = reinterpret_cast<int*>(sops + nops);
-  const RepSlot<T>& S = R.s[blockIdx.y];
+  REP_SLOT(S);
   double* val = S.pw;
   for (int i = threadIdx.x; i < nnodes; i += blockDim.x) sval[i] = val[i];
   for (int i = threadIdx.x; i < nops; i += blockDim.x) sops[i] = ops[i];
