@@ -59,8 +59,11 @@ def test_missing_seed_entry_raises(ops):
         s.try_update(0, int(gi[0]), int(gj[0]), 0)
 
 
+@pytest.mark.parametrize("graph", ["1", "0"])
 @pytest.mark.parametrize("name", ["s0", "s1", "s2", "s3", "s4", "s5", "conv", "c1"])
-def test_fast_stmf_matches_reference(fits, name):
+def test_fast_stmf_matches_reference(monkeypatch, fits, name, graph):
+    """Device-resident sweeps (CUDA graph, STMF_GRAPH=1) and the host-driven loop."""
+    monkeypatch.setenv("STMF_GRAPH", graph)
     c = fit_case(fits, name)
     R = pkg.MaskedMatrix(c["R"], c["M"])
     cfg = pkg.RunConfig(rank=int(c["rank"]), budget_sweeps=int(c["sweeps"]), epsilon=float(c["epsilon"]),
@@ -71,10 +74,13 @@ def test_fast_stmf_matches_reference(fits, name):
     assert np.array_equal(pair.U, c["U"]) and np.array_equal(pair.V, c["V"])
 
 
-def test_config1_full_100_sweeps_matches_reference_run():
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_config1_full_100_sweeps_matches_reference_run(monkeypatch, graph):
     """BASELINE.json configs[0] exactly as the survey ran the unmodified reference
     (100 sweeps, epsilon 0, seeds data 0 / mask 1 / fit 42):
-    3 078 993 attempts, final error 313.80609464110563 — reproduced bit for bit."""
+    3 078 993 attempts, final error 313.80609464110563 — reproduced bit for bit,
+    by the device-resident sweep graph and by the host-driven loop."""
+    monkeypatch.setenv("STMF_GRAPH", graph)
     from paper_2205_06619_b200 import gen
     R = gen.config1()
     cfg = pkg.RunConfig(rank=3, budget_sweeps=100, epsilon=0.0, seed=42)
@@ -103,8 +109,10 @@ def _f32_case(seed, m, n, r, frac):
 @pytest.mark.parametrize("seed,m,n,r,frac,sweeps", [(1, 30, 50, 3, 0.3, 4), (2, 64, 200, 5, 0.7, 2),
                                                      (3, 120, 90, 10, 0.5, 1)])
 def test_f32_fit_matches_restatement(monkeypatch, order, seed, m, n, r, frac, sweeps):
-    """Both phase-B item orders (line-major / group-major, STMF_GROUP_MAJOR)."""
+    """Both phase-B item orders (line-major / group-major, STMF_GROUP_MAJOR); the
+    line-major runs take the host-driven loop, the group-major ones the sweep graph."""
     monkeypatch.setenv("STMF_GROUP_MAJOR", order)
+    monkeypatch.setenv("STMF_GRAPH", order)
     work, U0 = _f32_case(seed, m, n, r, frac)
     with _ext.Session(work.values, work.mask, r) as s:
         s.set_factors(U0)
