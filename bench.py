@@ -285,8 +285,15 @@ def run_b200(args):
     peak, peak_src = peaks()
     achieved = b_launch / avg_s / 1e9 if nb else None
     l2_resident = 2 * N * (3 * s_bytes + 5) < 0.5 * 126e6
+    traffic, traffic_src = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_phaseB_traffic.json"))).get(str(args.config))
+        if tr:
+            traffic, traffic_src = tr["bytes"], tr["capture"]
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None, "traffic": None,
+                "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "stmf::k_phaseB (candidate evaluation: 2nd residuation + error, both rules)",
                 "bytes_per_launch": b_launch, "bytes_per_attempt": 2 * b_pass,
                 "evals_per_launch": evals_per_launch, "avg_launch_us": avg_s * 1e6, "launches": nb,
