@@ -284,6 +284,33 @@ struct Session : SessionBase {
   DevBuf<T> cx, xrow_dense;
   DevBuf<T> cmi, sq;  // CM^(-i) per k for the visited row; s_q of the batch's F-ULF evals
   bool inline_ulf = getenv("STMF_INLINE") ? atoi(getenv("STMF_INLINE")) != 0 : true;
+  // F-ULF hit partition of the visited row (k_hit_partition; needs the inline values)
+  bool split_ulf = inline_ulf && (getenv("STMF_SPLIT") ? atoi(getenv("STMF_SPLIT")) != 0 : false);
+  DevBuf<int32_t> hp_idx, hp_split;
+  DevBuf<T> hp_x, hp_t1, hp_t2;
+  DevBuf<uint8_t> hp_ag;
+  void row_partition() {
+    if (!split_ulf) return;
+    k_hit_partition<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p,
+                                                      xrow_dense.p, hp_idx.p, hp_x.p, hp_t1.p, hp_t2.p, hp_ag.p,
+                                                      hp_split.p);
+    LAUNCH_CK();
+  }
+  // the F-ULF side of phase B (CSR rows), on the hit-partitioned copy when enabled
+  SideB<T> side_ulf(u64* acc_p, int* chg_p) {
+    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_p, chg_p,
+                0, long_thr, group_major};
+    if (inline_ulf) {
+      sa.inl_base = cmi.p;
+      sa.inl_xr = xrow_dense.p;
+      sa.inl_s = sq.p;
+    }
+    if (split_ulf) {
+      sa.idx = hp_idx.p; sa.xv = hp_x.p; sa.t1 = hp_t1.p; sa.t2 = hp_t2.p; sa.ag = hp_ag.p;
+      sa.split = hp_split.p;
+    }
+    return sa;
+  }
   // batch scratch
   int Emax = 512;
   DevBuf<T> vbuf, ubufB, ubufA, vbufB, dtmpA, dtmpB;
@@ -427,9 +454,26 @@ struct Session : SessionBase {
       double entry_bytes = 2.0 * (double)N * (3 * sizeof(T) + 4 + 1);
       group_major = entry_bytes < 0.5 * (double)prop.l2CacheSize ? 1 : 0;
       if (const char* e = getenv("STMF_GROUP_MAJOR")) group_major = atoi(e);
-      CK(cudaFuncSetAttribute(k_phaseB<T, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-      CK(cudaFuncSetAttribute(k_phaseB<T, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-      CK(cudaFuncSetAttribute(k_phaseB<T, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+      // shared-memory carveout: phase B prefers L1 (0); STMF_CARVEOUT=c applies c to every
+      // kernel of a sweep instead (one L1/shared split: no reconfiguration between kernels)
+      int cv = getenv("STMF_CARVEOUT") ? atoi(getenv("STMF_CARVEOUT")) : -2;
+      int cvb = cv == -2 ? 0 : cv;
+      if (cvb >= -1) {
+        CK(cudaFuncSetAttribute(k_phaseB<T, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, cvb));
+        CK(cudaFuncSetAttribute(k_phaseB<T, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cvb));
+        CK(cudaFuncSetAttribute(k_phaseB<T, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cvb));
+      }
+      if (cv >= -1) {
+        const void* ks[] = {(const void*)k_phaseA<T>, (const void*)k_phaseA_urf_seed_chk<T>,
+                            (const void*)k_cand_row<T, 1>, (const void*)k_cand_row<T, 4>,
+                            (const void*)k_residuals_delta_multi<T>, (const void*)k_sort_delta_multi<T>,
+                            (const void*)k_merge_delta_multi<T>, (const void*)k_pw_leaves8_multi<T>,
+                            (const void*)k_pw_combine_multi_smem<T>, (const void*)k_product2<T>,
+                            (const void*)k_scores<T>, (const void*)k_line_stats<T>, (const void*)k_g_commit<T>,
+                            (const void*)k_g_decide<T>, (const void*)k_g_decide_esc<T>, (const void*)k_g_zero,
+                            (const void*)k_g_row_begin, (const void*)k_g_row_end, (const void*)k_g_fb_check};
+        for (const void* f : ks) CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+      }
       CK(cudaFuncSetAttribute(k_pw_combine_multi_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kCombineSmem));
     }
@@ -457,6 +501,9 @@ struct Session : SessionBase {
     ckeys.alloc(n); ckeys2.alloc(n); cvals.alloc(n); cperm.alloc(n);
     cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
     cmi.alloc((size_t)rank * n); sq.alloc(n);
+    if (split_ulf) {
+      hp_idx.alloc(N); hp_x.alloc(N); hp_t1.alloc(N); hp_t2.alloc(N); hp_ag.alloc(N); hp_split.alloc(m);
+    }
     vbuf.alloc((size_t)Emax * n); ubufB.alloc((size_t)Emax * m);
     ubufA.alloc((size_t)Emax * m); vbufB.alloc((size_t)Emax * n);
     dtmpA.alloc(m); dtmpB.alloc(n);
@@ -869,6 +916,7 @@ struct Session : SessionBase {
                                        colhist.p, cj.p, ck.p, cx.p, xrow_dense.p, i, cm1.p, cm2.p, cmarg.p, cmi.p,
                                        nullptr, nullptr);
       LAUNCH_CK();
+      row_partition();
       return nc;
     }
     k_cand_keys<<<nblk(nc, 256), 256, 0, st>>>(nc, col_idx.p + beg, score.p, ckeys.p, cvals.p);
@@ -882,6 +930,7 @@ struct Session : SessionBase {
     LAUNCH_CK();
     dense_row(i);
     row_cmi(i);
+    row_partition();
     return nc;
   }
 
@@ -922,13 +971,7 @@ struct Session : SessionBase {
                                                 chg_urf);
     LAUNCH_CK();
     int ng = (E + kEG - 1) / kEG;
-    SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, acc_ulf, chg_ulf,
-                0, long_thr, group_major};
-    if (inline_ulf) {
-      sa.inl_base = cmi.p;
-      sa.inl_xr = xrow_dense.p;
-      sa.inl_s = sq.p;
-    }
+    SideB<T> sa = side_ulf(acc_ulf, chg_ulf);
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
                 0, long_thr, group_major};
     if (profiling) CK(cudaEventRecord(ev_b0, st));
@@ -1309,6 +1352,7 @@ struct Session : SessionBase {
       kern<<<1, kCandThreads, 0, st>>>(0, n, rank, col_idx.p, xr.p, agr.p, score.p, colhist.p, cj.p, ck.p, cx.p,
                                        xrow_dense.p, 0, cm1.p, cm2.p, cmarg.p, cmi.p, c, row_ptr.p);
     }
+    row_partition();
     dr = cap_end(b_row);
     cudaGraph_t b_batch = add_cond(b_row, dr, h_batch, cudaGraphCondTypeWhile);
 
@@ -1324,13 +1368,7 @@ struct Session : SessionBase {
                                                     ubufA.p, nullptr, c, bstate.p);
     if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c);
     {
-      SideB<T> sa{m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, vbuf.p, n, Ut.p, ubufB.p, nullptr, nullptr,
-                  0, long_thr, group_major};
-      if (inline_ulf) {
-        sa.inl_base = cmi.p;
-        sa.inl_xr = xrow_dense.p;
-        sa.inl_s = sq.p;
-      }
+      SideB<T> sa = side_ulf(nullptr, nullptr);
       SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, nullptr, nullptr,
                   0, long_thr, group_major};
       unsigned gb = (unsigned)nsm * (sizeof(T) == 8 && unroll > 1 ? 2 : 3);
@@ -1562,6 +1600,7 @@ struct Session : SessionBase {
     CK(cudaMemcpyAsync(cx.p, xr.p + p, sizeof(T), cudaMemcpyDeviceToDevice, st));
     dense_row(i);
     row_cmi(i);
+    row_partition();
     eval_batch(i, 0, 1);
     ssync();
     double fv;

@@ -906,7 +906,49 @@ struct SideB {
   const T* inl_base = nullptr;
   const T* inl_xr = nullptr;
   const T* inl_s = nullptr;
+  // F-ULF hit partition of the visited row (k_hit_partition): xv/idx/t1/t2/ag then
+  // hold each line's entries reordered [columns not given in row i | the others], and
+  // split[L] is the boundary (null: no partition)
+  const int32_t* split = nullptr;
 };
+
+// Per row visit: reorder each CSR row's entries into [columns not given in row i |
+// columns given in row i] (order inside the segments is irrelevant: minima are exact
+// and the error partials' bound holds for any summation order), with the product
+// caches, so phase B's F-ULF evals share one value on the first segment.
+template <typename T>
+__global__ void k_hit_partition(int64_t m, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                const T* __restrict__ xr, const T* __restrict__ t1, const T* __restrict__ t2,
+                                const uint8_t* __restrict__ ag, const T* __restrict__ xrow_dense,
+                                int32_t* __restrict__ pidx, T* __restrict__ px, T* __restrict__ pt1,
+                                T* __restrict__ pt2, uint8_t* __restrict__ pag, int32_t* __restrict__ split) {
+  int lane = threadIdx.x & 31;
+  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned lt = (1u << lane) - 1;
+  for (int64_t a = w; a < m; a += nw) {
+    int beg = (int)row_ptr[a], end = (int)row_ptr[a + 1];
+    int lo = beg, hi = end;
+    for (int p0 = beg; p0 < end; p0 += 32) {
+      int p = p0 + lane;
+      bool ok = p < end;
+      int c = ok ? col_idx[p] : 0;
+      bool hit = ok && xrow_dense[c] != tinf<T>();
+      unsigned bh = __ballot_sync(0xffffffffu, hit), bn = __ballot_sync(0xffffffffu, ok && !hit);
+      if (ok) {
+        int d = hit ? hi - 1 - __popc(bh & lt) : lo + __popc(bn & lt);
+        pidx[d] = c;
+        px[d] = xr[p];
+        pt1[d] = t1[p];
+        pt2[d] = t2[p];
+        pag[d] = ag[p];
+      }
+      lo += __popc(bn);
+      hi -= __popc(bh);
+    }
+    if (lane == 0) split[a] = lo;
+  }
+}
 
 template <int EG, typename V>
 __device__ __forceinline__ V lane_pick(const V (&a)[EG], int q) {
@@ -976,9 +1018,103 @@ __device__ __forceinline__ V warp_reduce8(const V (&v)[kEG], int lane) {
   return op(r, shfl_xor(r, 1));
 }
 
+// Pass 1 over entries [lo, hi) of a line: per-eval line minima of x - v'.  SHARED
+// (F-ULF entries whose column is not given in row i, VM 2 only): v' is the group's
+// base value for every eval, so one minimum mn0 serves all 8 evals.
+template <typename T, int VM, bool SHARED>
+__device__ __forceinline__ void pass1_seg(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+                                          const T* __restrict__ base, const T (&s)[kEG], int lo, int hi, int lane,
+                                          T (&mn)[kEG], T& mn0) {
+  constexpr int EG = kEG;
+  // U entries per lane per iteration: their idx -> vin gathers are in flight
+  // together (the loop is latency-bound otherwise); missing slots use x = +inf
+  constexpr int U = sizeof(T) == 8 ? 2 : 4;
+  const T* __restrict__ xv = S.xv;
+  const int32_t* __restrict__ idx = S.idx;
+  for (int p0 = lo + lane; p0 < hi; p0 += 32 * U) {
+    T x[U];
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int p = p0 + 32 * u;
+      bool ok = p < hi;
+      x[u] = ok ? xv[p] : tinf<T>();
+      c[u] = ok ? idx[p] : 0;
+    }
+    if (SHARED) {
+#pragma unroll
+      for (int u = 0; u < U; u++) mn0 = vmin(mn0, sub_rn(x[u], base[c[u]]));
+    } else {
+      T v[U][EG];
+#pragma unroll
+      for (int u = 0; u < U; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x[u], v[u][q]));
+    }
+  }
+}
+
+// Pass 2 over entries [lo, hi): per-eval error partials with the new line values mn.
+// |x - max(Q, w)| == |min(x - Q, x - w)| exactly (x - . is monotone under rounding).
+template <typename T, int UNR, int VM, bool SHARED>
+__device__ __forceinline__ void pass2_seg(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+                                          const T* __restrict__ base, const T (&s)[kEG], const int (&kq)[kEG],
+                                          int lo, int hi, int lane, const T (&mn)[kEG], double (&part)[kEG]) {
+  constexpr int EG = kEG, U2 = UNR;
+  const T* __restrict__ xv = S.xv;
+  const int32_t* __restrict__ idx = S.idx;
+  for (int p0 = lo + lane; p0 < hi; p0 += 32 * U2) {
+    T x[U2], a1[U2], a2[U2];
+    int a[U2], c[U2];
+#pragma unroll
+    for (int u = 0; u < U2; u++) {
+      int p = p0 + 32 * u;
+      bool ok = p < hi;
+      int pp = ok ? p : lo;
+      x[u] = xv[pp];
+      c[u] = idx[pp];
+      a1[u] = S.t1[pp];
+      a2[u] = S.t2[pp];
+      a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the segment (contributes 0)
+    }
+    T v[U2][EG];
+    if (SHARED) {
+#pragma unroll
+      for (int u = 0; u < U2; u++) {
+        T b = base[c[u]];
+#pragma unroll
+        for (int q = 0; q < EG; q++) v[u][q] = b;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U2; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U2; u++) {
+      if (a[u] < 0) continue;
+      if (VM >= 1) {
+        T r1 = sub_rn(x[u], (a[u] == kq[0]) ? a2[u] : a1[u]);
+#pragma unroll
+        for (int q = 0; q < EG; q++)
+          part[q] = __dadd_rn(part[q], (double)vabs(vmin(r1, sub_rn(x[u], add_rn(mn[q], v[u][q])))));
+      } else {
+#pragma unroll
+        for (int q = 0; q < EG; q++) {
+          T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
+          T pm = vmax(Q, add_rn(mn[q], v[u][q]));
+          part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
+        }
+      }
+    }
+  }
+}
+
 // VM: 0 = planar, per-eval k; 1 = planar, one k for the group (Q shared per
-// entry); 2 = one k, F-ULF values recomputed inline (no per-eval gathers).
-// Entry offsets are 32-bit (N < 2^31 is checked at session creation).
+// entry); 2 = one k, F-ULF values recomputed inline (no per-eval gathers), and with
+// a hit partition (S.split) the entries whose column is not given in row i share
+// one value for all evals.  Entry offsets are 32-bit (N < 2^31 per device).
 template <typename T, int UNR, int VM>
 __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g, int e0, int ne,
                                             const int (&kq)[kEG], int lane, int* __restrict__ flags, int F,
@@ -998,8 +1134,7 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
     for (int q = 0; q < EG; q++) s[q] = S.inl_s[e0 + (q < ne ? q : ne - 1)];
   }
   const int beg = (int)S.ptr[L], end = (int)S.ptr[L + 1];
-  const T* __restrict__ xv = S.xv;
-  const int32_t* __restrict__ idx = S.idx;
+  const int sp = (VM == 2 && S.split) ? S.split[L] : beg;  // [beg, sp): shared values
   T mn[EG];
   if (S.mode == 2) {
     // sharded F-URF second half: the line values are the all-reduced minima
@@ -1008,27 +1143,11 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   } else {
 #pragma unroll
     for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-    // U entries per lane per iteration: their idx -> vin gathers are in flight
-    // together (the loop is latency-bound otherwise); missing slots use x = +inf
-    constexpr int U = sizeof(T) == 8 ? 2 : 4;  // pass 1 is cheap in registers: always unrolled
-    for (int p0 = beg + lane; p0 < end; p0 += 32 * U) {
-      T x[U];
-      int c[U];
+    T mn0 = tinf<T>();
+    if (VM == 2 && sp > beg) pass1_seg<T, VM, true>(S, pl, base, s, beg, sp, lane, mn, mn0);
+    pass1_seg<T, VM, false>(S, pl, base, s, sp, end, lane, mn, mn0);
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        int p = p0 + 32 * u;
-        bool ok = p < end;
-        x[u] = ok ? xv[p] : tinf<T>();
-        c[u] = ok ? idx[p] : 0;
-      }
-      T v[U][EG];
-#pragma unroll
-      for (int u = 0; u < U; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
-#pragma unroll
-      for (int u = 0; u < U; u++)
-#pragma unroll
-        for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x[u], v[u][q]));
-    }
+    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], mn0);
     T r = warp_reduce8<T, false>(mn, lane);
 #pragma unroll
     for (int q = 0; q < EG; q++) mn[q] = __shfl_sync(0xffffffffu, r, q << 2);
@@ -1043,43 +1162,8 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   double part[EG];
 #pragma unroll
   for (int q = 0; q < EG; q++) part[q] = 0.0;
-  // |x - max(Q, w)| == |min(x - Q, x - w)| exactly (x - . is monotone under rounding)
-  constexpr int U2 = UNR;
-  for (int p0 = beg + lane; p0 < end; p0 += 32 * U2) {
-    T x[U2], a1[U2], a2[U2];
-    int a[U2], c[U2];
-#pragma unroll
-    for (int u = 0; u < U2; u++) {
-      int p = p0 + 32 * u;
-      bool ok = p < end;
-      int pp = ok ? p : beg;
-      x[u] = xv[pp];
-      c[u] = idx[pp];
-      a1[u] = S.t1[pp];
-      a2[u] = S.t2[pp];
-      a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the line (contributes 0)
-    }
-    T v[U2][EG];
-#pragma unroll
-    for (int u = 0; u < U2; u++) eval_vals<T, VM>(S.inl_xr, base, pl, s, c[u], v[u]);
-#pragma unroll
-    for (int u = 0; u < U2; u++) {
-      if (a[u] < 0) continue;
-      if (VM >= 1) {
-        T r1 = sub_rn(x[u], (a[u] == kq[0]) ? a2[u] : a1[u]);
-#pragma unroll
-        for (int q = 0; q < EG; q++)
-          part[q] = __dadd_rn(part[q], (double)vabs(vmin(r1, sub_rn(x[u], add_rn(mn[q], v[u][q])))));
-      } else {
-#pragma unroll
-        for (int q = 0; q < EG; q++) {
-          T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
-          T pm = vmax(Q, add_rn(mn[q], v[u][q]));
-          part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
-        }
-      }
-    }
-  }
+  if (VM == 2 && sp > beg) pass2_seg<T, UNR, VM, true>(S, pl, base, s, kq, beg, sp, lane, mn, part);
+  pass2_seg<T, UNR, VM, false>(S, pl, base, s, kq, sp, end, lane, mn, part);
   double pv = warp_reduce8<double, true>(part, lane);
   int q = (lane >> 2) & 7;
   if ((lane & 3) == 0 && q < ne) {

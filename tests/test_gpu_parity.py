@@ -131,9 +131,12 @@ def test_f32_fit_matches_restatement(monkeypatch, order, seed, m, n, r, frac, sw
 
 
 @pytest.mark.parametrize("order", ["0", "1"])
-def test_f64_fit_matches_restatement_lognormal(monkeypatch, order):
-    """A reduced config-2 shape (log2(1+lognormal), 50% hidden) vs the oracle."""
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_f64_fit_matches_restatement_lognormal(monkeypatch, order, split):
+    """A reduced config-2 shape (log2(1+lognormal), 50% hidden) vs the oracle, with and
+    without the F-ULF hit partition (STMF_SPLIT)."""
     monkeypatch.setenv("STMF_GROUP_MAJOR", order)
+    monkeypatch.setenv("STMF_SPLIT", split)
     rng = np.random.default_rng(5)
     X = np.log2(1 + rng.lognormal(0, 1, (60, 140)))
     from paper_2205_06619_b200 import gen
