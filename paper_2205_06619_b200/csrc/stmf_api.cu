@@ -1371,8 +1371,8 @@ struct Session : SessionBase {
       SideB<T> sa = side_ulf(nullptr, nullptr);
       SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, nullptr, nullptr,
                   0, long_thr, group_major};
-      unsigned gb = (unsigned)nsm * (sizeof(T) == 8 && unroll > 1 ? 2 : 3);
-      if (unroll >= 4) gb = (unsigned)nsm * 2;
+      // one wave of resident CTAs (the kernel's launch bounds)
+      unsigned gb = (unsigned)nsm * (unroll >= 4 ? 2 : sizeof(T) == 4 ? kPhaseBCtasF32 : unroll > 1 ? 2 : kPhaseBCtasF64);
       if (unroll >= 4)
         k_phaseB<T, 4><<<gb, 256, 0, st>>>(sa, sb, 0, nullptr, flags.p, F, exact_limit, c, bstate.p, ck.p);
       else if (unroll == 2)

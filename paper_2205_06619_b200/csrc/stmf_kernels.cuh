@@ -1209,6 +1209,15 @@ __device__ __forceinline__ void phaseB_item(const SideB<T>& S, int64_t it, int E
   else phaseB_body<T, UNR, 1>(S, L, g, e0, ne, kq, lane, flags, F, exact_limit);
 }
 
+#ifndef STMF_PHASEB_CTAS_F32
+#define STMF_PHASEB_CTAS_F32 4
+#endif
+constexpr int kPhaseBCtasF32 = STMF_PHASEB_CTAS_F32;  // resident phase-B CTAs per SM (binary32)
+#ifndef STMF_PHASEB_CTAS_F64
+#define STMF_PHASEB_CTAS_F64 3
+#endif
+constexpr int kPhaseBCtasF64 = STMF_PHASEB_CTAS_F64;  // (binary64, one entry per lane per iteration)
+
 // graph mode: the batch window and the result slots of bstate
 // ([flags: 4 int][acc: 4E u64][chg: 2E int]) from the control block
 template <typename T>
@@ -1224,7 +1233,7 @@ __device__ __forceinline__ void batch_from_ctl(const DevCtl* g, u64* bst, SideB<
 // rows (rc + error), items [A, A+B) F-URF evals on CSC columns (rr + error).
 // UNR = entries per lane per loop iteration (memory-level parallelism vs registers)
 template <typename T, int UNR>
-__global__ void __launch_bounds__(256, UNR > 2 ? 2 : (sizeof(T) == 8 && UNR > 1 ? 2 : 3))
+__global__ void __launch_bounds__(256, UNR > 2 ? 2 : (sizeof(T) == 8 && UNR > 1 ? 2 : (sizeof(T) == 4 ? kPhaseBCtasF32 : kPhaseBCtasF64)))
 k_phaseB(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, int* __restrict__ flags, int F,
          double exact_limit, const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr,
          const int32_t* __restrict__ ck = nullptr) {
