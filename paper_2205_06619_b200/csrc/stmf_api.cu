@@ -364,6 +364,9 @@ struct Session : SessionBase {
 
   ~Session() override {
     graph_destroy();
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st2) cudaStreamDestroy(st2);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
@@ -1285,6 +1288,22 @@ struct Session : SessionBase {
     return cp.conditional.phGraph_out[0];
   }
 
+  cudaStream_t st2 = nullptr;          // second capture stream (graph branches)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // pairwise-tree combine of a replica round read from the device descriptor
+  void launch_combine(int ys, RepRound<T>* rp_, cudaStream_t s_) {
+    RepRound<T> none{};
+    int nops = (int)pw.lvl_nodes.size();
+    size_t sm = sizeof(double) * (size_t)((pw.nnodes + 1) & ~1) + sizeof(int4) * (size_t)nops +
+                sizeof(int) * (size_t)(pw.H + 1);
+    if (sm <= kCombineSmem)
+      k_pw_combine_multi_smem<T><<<dim3(1, ys), 1024, sm, s_>>>(pw.H, pw.nnodes, nops, pw_lvloff.p, pw_ops.p, none,
+                                                                rp_);
+    else
+      k_pw_combine_multi<T><<<dim3(1, ys), 1024, 0, s_>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p,
+                                                           none, rp_);
+  }
+
   GBufs<T> gbufs() {
     GBufs<T> B{};
     B.bst = bstate.p; B.ck = ck.p;
@@ -1313,6 +1332,11 @@ struct Session : SessionBase {
 
   void graph_build() {
     graph_destroy();
+    if (!st2) {
+      CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
     if (!dctl.p) {
       dctl.alloc(1);
       CK(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
@@ -1397,17 +1421,7 @@ struct Session : SessionBase {
       int nl = (int)pw.loff.size();
       k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), kSlots), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p,
                                                                                      pw_lnode.p, none, rp_);
-      if (pw.H > 0) {
-        int nops = (int)pw.lvl_nodes.size();
-        size_t sm = sizeof(double) * (size_t)((pw.nnodes + 1) & ~1) + sizeof(int4) * (size_t)nops +
-                    sizeof(int) * (size_t)(pw.H + 1);
-        if (sm <= kCombineSmem)
-          k_pw_combine_multi_smem<T><<<dim3(1, kSlots), 1024, sm, st>>>(pw.H, pw.nnodes, nops, pw_lvloff.p,
-                                                                        pw_ops.p, none, rp_);
-        else
-          k_pw_combine_multi<T><<<dim3(1, kSlots), 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p,
-                                                                   pw_right.p, none, rp_);
-      }
+      if (pw.H > 0) launch_combine(kSlots, rp_, st);
       k_g_fb_check<<<1, 1, 0, st>>>(c, d_pwout.p, h_fb);
       de = cap_end(b_esc);
       cudaGraph_t b_fb = add_cond(b_esc, de, h_fb, cudaGraphCondTypeIf);
@@ -1438,6 +1452,24 @@ struct Session : SessionBase {
       const int* kc = &c->cache_k;
       k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
                                            t1r.p, t2r.p, agr.p, a2r.p, kc);
+      if (!kExact) {
+        // fp64 direct accept: the numpy replica of the committed state (residuals from
+        // the new CSR product) on a second branch, overlapped with the remaining caches
+        CK(cudaEventRecord(ev_fork, st));
+        CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+        RepRound<T> none{};
+        RepRound<T>* rp_ = d_rr.p;
+        k_res_from_product<T><<<(unsigned)nsm * 8, 256, 0, st2>>>(c, N, xr.p, t1r.p, res_cur.p, rp_);
+        k_sort_delta_multi<T><<<dim3(2, 1), kSortThreads, 0, st2>>>(none, rp_);
+        unsigned mt = (unsigned)((N + kMergeTile - 1) / kMergeTile);
+        k_merge_delta_multi<T><<<dim3(mt, 1), 256, 0, st2>>>(N, S_cur.p, none, rp_);
+        int nl = (int)pw.loff.size();
+        k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), 1), 256, 0, st2>>>(nl, pw_loff.p, pw_llen.p,
+                                                                                    pw_lnode.p, none, rp_);
+        if (pw.H > 0) launch_combine(1, rp_, st2);
+        k_g_adopt<T><<<gc, 256, 0, st2>>>(c, B, N, res_cur.p, S_cur.p);
+        CK(cudaEventRecord(ev_join, st2));
+      }
       k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
                                            t1c.p, t2c.p, agc.p, a2c.p, kc);
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
@@ -1446,6 +1478,7 @@ struct Session : SessionBase {
                                                         kc, m, n);
       k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
                                                         kc, n, m);
+      if (!kExact) CK(cudaStreamWaitEvent(st, ev_join, 0));
       cap_end(b_acc);
     }
     cap_begin(b_row, dr);
@@ -1455,46 +1488,87 @@ struct Session : SessionBase {
     graph_epoch = ptr_epoch;
   }
 
-  // one sweep as one graph launch; returns false if the graph path does not apply
+  // numpy value of the current state from scratch (residuals, full sort, pairwise
+  // tree) into res_cur / S_cur, without swapping buffers
+  double exact_current_objective() {
+    k_residuals<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, t1r.p, t2r.p, agr.p, 0, Ut.p, 1,
+                                                    V.p, 1, res_cur.p);
+    LAUNCH_CK();
+    size_t bytes = cubtmp_bytes;
+    CK(cub::DeviceRadixSort::SortKeys(cubtmp.p, bytes, res_cur.p, S_cur.p, (int64_t)N, 0, 63, st));
+    g_cub_calls++;
+    int nl = (int)pw.loff.size();
+    k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, pw_loff.p, pw_llen.p, pw_lnode.p, S_cur.p,
+                                                            slots[0].pw.p);
+    LAUNCH_CK();
+    if (pw.H > 0) {
+      k_pw_combine<<<1, 1024, 0, st>>>(pw.H, pw_lvloff.p, pw_lvlnodes.p, pw_left.p, pw_right.p, slots[0].pw.p);
+      LAUNCH_CK();
+    }
+    CK(cudaMemcpyAsync(h_pwv, slots[0].pw.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    ssync();
+    return h_pwv[0];
+  }
+
+  // one sweep as (normally) one graph launch
   void graph_sweep(RunState& R) {
     if (!g_exec || graph_epoch != ptr_epoch || graph_prof != profiling) {
       graph_prof = profiling;
       graph_build();
     }
     DevCtl& h = *h_ctl;
-    std::memset(&h, 0, sizeof(DevCtl));
-    h.err = err;
-    h.traj_cap = m + 1;
-    h.sweep = (double)R.cur_sweep;
-    h.sched_scale = sched_scale; h.sched_growth = sched_growth; h.sched_add = sched_add;
-    h.batch_floor = batch_floor; h.Emax = Emax; h.first0 = batch_sched[0];
-    h.cache_k = -1;
-    h.tb0 = 0;
-    CK(cudaMemcpyAsync(dctl.p, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
-    CK(cudaGraphLaunch(g_exec, st));
-    CK(cudaMemcpyAsync(h_ctl, dctl.p, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_traj_t.data(), d_traj_t.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_traj_e.data(), d_traj_e.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
-    ssync();
-    if (h.error == 1) fail(STMF_ERR_NUMERIC, "decision bound violated (device decision)");
-    if (h.error == 2) fail(STMF_ERR_CAPACITY, "device trajectory capacity exceeded");
-    if (h.error == 3) fail(STMF_ERR_NUMERIC, "exact objective window violated (graph sweep, grid 2^-%d)", F);
-    for (long long t = 0; t < h.traj_len; t++) traj_append(R, h_traj_t[t], h_traj_e[t]);
-    err = h.err;
-    R.attempts += h.attempts;
-    R.accepts += h.accepts;
-    R.visits += h.visits;
-    R.evaluated += h.evaluated;
-    n_escalations += h.escalations;
-    n_product_passes += h.accepts;
-    phaseB_launches += h.batches;
-    if (graph_prof) {
-      phaseB_ns += (long long)h.phaseB_ns;
-      phaseB_timed += h.batches;
+    long long start = 0;
+    for (;;) {
+      std::memset(&h, 0, sizeof(DevCtl));
+      h.err = err;
+      h.start_row = start;
+      // STMF_DIRECT_CAP (tests): a smaller limit forces the full-replica resumption
+      h.direct_cap = getenv("STMF_DIRECT_CAP") ? std::min(kDeltaCap, atoi(getenv("STMF_DIRECT_CAP"))) : kDeltaCap;
+      h.traj_cap = m + 1;
+      h.sweep = (double)R.cur_sweep;
+      h.sched_scale = sched_scale; h.sched_growth = sched_growth; h.sched_add = sched_add;
+      h.batch_floor = batch_floor; h.Emax = Emax; h.first0 = batch_sched[0];
+      h.cache_k = -1;
+      h.tb0 = 0;
+      CK(cudaMemcpyAsync(dctl.p, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+      CK(cudaGraphLaunch(g_exec, st));
+      CK(cudaMemcpyAsync(h_ctl, dctl.p, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_traj_t.data(), d_traj_t.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_traj_e.data(), d_traj_e.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, st));
+      ssync();
+      if (h.error == 1) fail(STMF_ERR_NUMERIC, "decision bound violated (device decision)");
+      if (h.error == 2) fail(STMF_ERR_CAPACITY, "device trajectory capacity exceeded");
+      if (h.error == 3) fail(STMF_ERR_NUMERIC, "exact objective window violated (graph sweep, grid 2^-%d)", F);
+      for (long long t = 0; t < h.traj_len; t++) traj_append(R, h_traj_t[t], h_traj_e[t]);
+      err = h.err;
+      R.attempts += h.attempts;
+      R.accepts += h.accepts;
+      R.visits += h.visits;
+      R.evaluated += h.evaluated;
+      n_escalations += h.escalations;
+      n_product_passes += h.accepts;
+      phaseB_launches += h.batches;
+      if (graph_prof) {
+        phaseB_ns += (long long)h.phaseB_ns;
+        phaseB_timed += h.batches;
+      }
+      // kernel nodes executed: row (3), batch (5 + tick), escalation round (7 + 1), accept (6, +7 fp64)
+      g_launches += h.visits * 3 + h.batches * (5 + (graph_prof ? 1 : 0)) + h.esc_rounds * 8 +
+                    h.accepts * (kExact ? 6 : 13);
+      if (h.error == 4) {
+        // a direct accept changed more than kDeltaCap residuals: its numpy value from a
+        // full replica of the committed state, then the sweep resumes at the next row
+        double fr = exact_current_objective();
+        if (!(fr < h.err_prev)) fail(STMF_ERR_NUMERIC, "decision bound violated: replica=%.17g err=%.17g", fr,
+                                     h.err_prev);
+        err = fr;
+        R.te[R.len - 1] = fr;
+        start = h.i;
+        if (start < m) continue;
+      }
+      break;
     }
-    // kernel nodes executed: row (3), batch (5 + tick), escalation round (7 + 1), accept (6)
-    g_launches += h.visits * 3 + h.batches * (5 + (graph_prof ? 1 : 0)) + h.esc_rounds * 8 + h.accepts * 6;
-    if (h.accepts) dirty = false;
+    dirty = false;
     cache_k = -1;
   }
 

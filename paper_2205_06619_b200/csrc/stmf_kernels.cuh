@@ -46,6 +46,10 @@ struct DevCtl {
   // run bookkeeping
   long long attempts, accepts, visits, evaluated, escalations, traj_len, traj_cap;
   long long batches, esc_rounds;
+  int direct;            // accept committed before its numpy replica (certain accept)
+  long long start_row;   // first row of this graph launch (resumption after error 4)
+  int direct_cap;        // changed-entry limit of a direct accept's delta replica
+  double err_prev;       // err before a direct accept (its replica must be below)
   unsigned long long tb0, phaseB_ns;  // graph-mode phase-B timing (%globaltimer)
   double sweep;          // trajectory time stamp of this sweep
   int error;             // 1: decision bound violated, 2: trajectory capacity

@@ -59,11 +59,14 @@ def test_missing_seed_entry_raises(ops):
         s.try_update(0, int(gi[0]), int(gj[0]), 0)
 
 
-@pytest.mark.parametrize("graph", ["1", "0"])
+@pytest.mark.parametrize("graph", ["1", "0", "cap"])
 @pytest.mark.parametrize("name", ["s0", "s1", "s2", "s3", "s4", "s5", "conv", "c1"])
 def test_fast_stmf_matches_reference(monkeypatch, fits, name, graph):
-    """Device-resident sweeps (CUDA graph, STMF_GRAPH=1) and the host-driven loop."""
-    monkeypatch.setenv("STMF_GRAPH", graph)
+    """Device-resident sweeps (CUDA graph, STMF_GRAPH=1), the host-driven loop, and the
+    graph with every direct accept resolved by the host's full replica (STMF_DIRECT_CAP)."""
+    monkeypatch.setenv("STMF_GRAPH", "0" if graph == "0" else "1")
+    if graph == "cap":
+        monkeypatch.setenv("STMF_DIRECT_CAP", "1")
     c = fit_case(fits, name)
     R = pkg.MaskedMatrix(c["R"], c["M"])
     cfg = pkg.RunConfig(rank=int(c["rank"]), budget_sweeps=int(c["sweeps"]), epsilon=float(c["epsilon"]),
