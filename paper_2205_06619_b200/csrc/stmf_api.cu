@@ -1361,9 +1361,15 @@ struct Session : SessionBase {
     CK(cudaGraphConditionalHandleCreate(&h_row, g_top, 0, 0));
     std::vector<cudaGraphNode_t> d0;
     cap_begin(g_top, d0);
+    if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 5);
     k_g_sweep_begin<<<1, 1, 0, st>>>(c, m, h_row);
     d0 = cap_end(g_top);
     cudaGraph_t b_row = add_cond(g_top, d0, h_row, cudaGraphCondTypeWhile);
+    if (graph_prof) {
+      cap_begin(g_top, d0);
+      k_g_tick<<<1, 1, 0, st>>>(c, 6);
+      cap_end(g_top);
+    }
 
     // ---- row body
     CK(cudaGraphConditionalHandleCreate(&h_batch, b_row, 0, 0));
@@ -1390,7 +1396,7 @@ struct Session : SessionBase {
                                                    ubufA.p, nullptr, c, bstate.p);
     k_phaseA_urf_seed_chk<T><<<Emax, 128, 0, st>>>(m, 0, 0, cj.p, ck.p, cx.p, Ut.p, col_ptr.p, row_idx.p, xc.p,
                                                     ubufA.p, nullptr, c, bstate.p);
-    if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c);
+    if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 0);
     {
       SideB<T> sa = side_ulf(nullptr, nullptr);
       SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, nullptr, nullptr,
@@ -1411,6 +1417,7 @@ struct Session : SessionBase {
       CK(cudaGraphConditionalHandleCreate(&h_fb, b_esc, 0, 0));
       std::vector<cudaGraphNode_t> de;
       cap_begin(b_esc, de);
+      if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 1);
       RepRound<T> none{};
       RepRound<T>* rp_ = d_rr.p;
       k_residuals_delta_multi<T><<<dim3(nblk(N, 256), kSlots), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p,
@@ -1436,16 +1443,20 @@ struct Session : SessionBase {
         cap_end(b_fb);
       }
       cap_begin(b_esc, de);
+      if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 2);
       k_g_decide_esc<T><<<1, kDecideThreads, 0, st>>>(c, B, h_batch, h_acc, h_esc);
       cap_end(b_esc);
     }
 
     // ---- accept (after the batch loop)
     cudaGraph_t b_acc = add_cond(b_row, dr, h_acc, cudaGraphCondTypeIf);
+    cudaGraphConditionalHandle h_fb1 = 0;
+    unsigned gc = (unsigned)nsm * 4;
+    if (!kExact) CK(cudaGraphConditionalHandleCreate(&h_fb1, b_acc, 0, 0));
     {
       std::vector<cudaGraphNode_t> da;
       cap_begin(b_acc, da);
-      unsigned gc = (unsigned)nsm * 4;
+      if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 3);
       k_g_commit<T><<<gc, 256, 0, st>>>(c, B, Ut.p, V.p, Urm.p, Vcm.p, rp, N, kExact ? nullptr : res_cur.p,
                                         kExact ? nullptr : S_cur.p);
       unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
@@ -1467,7 +1478,7 @@ struct Session : SessionBase {
         k_pw_leaves8_multi<T><<<dim3(nblk((int64_t)nl * 8, 256), 1), 256, 0, st2>>>(nl, pw_loff.p, pw_llen.p,
                                                                                     pw_lnode.p, none, rp_);
         if (pw.H > 0) launch_combine(1, rp_, st2);
-        k_g_adopt<T><<<gc, 256, 0, st2>>>(c, B, N, res_cur.p, S_cur.p);
+        k_g_fb1_check<<<1, 1, 0, st2>>>(c, d_pwout.p, h_fb1);
         CK(cudaEventRecord(ev_join, st2));
       }
       k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
@@ -1479,6 +1490,19 @@ struct Session : SessionBase {
       k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
                                                         kc, n, m);
       if (!kExact) CK(cudaStreamWaitEvent(st, ev_join, 0));
+      da = cap_end(b_acc);
+      if (!kExact) {
+        cudaGraph_t b_fb1 = add_cond(b_acc, da, h_fb1, cudaGraphCondTypeIf);
+        std::vector<cudaGraphNode_t> df;
+        cap_begin(b_fb1, df);
+        full_sort(slots[0]);
+        pw_sum(slots[0]);
+        k_g_fb1_fix<<<1, 1, 0, st>>>(slots[0].pw.p, d_pwout.p);
+        cap_end(b_fb1);
+      }
+      cap_begin(b_acc, da);
+      if (!kExact) k_g_adopt<T><<<gc, 256, 0, st>>>(c, B, N, res_cur.p, S_cur.p);
+      if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 4);
       cap_end(b_acc);
     }
     cap_begin(b_row, dr);
@@ -1514,7 +1538,9 @@ struct Session : SessionBase {
   void graph_sweep(RunState& R) {
     if (!g_exec || graph_epoch != ptr_epoch || graph_prof != profiling) {
       graph_prof = profiling;
+      double t0 = now_s();
       graph_build();
+      if (getenv("STMF_GRAPH_STATS")) fprintf(stderr, "[stmf graph] build %.1f ms\n", (now_s() - t0) * 1e3);
     }
     DevCtl& h = *h_ctl;
     long long start = 0;
@@ -1555,6 +1581,12 @@ struct Session : SessionBase {
       // kernel nodes executed: row (3), batch (5 + tick), escalation round (7 + 1), accept (6, +7 fp64)
       g_launches += h.visits * 3 + h.batches * (5 + (graph_prof ? 1 : 0)) + h.esc_rounds * 8 +
                     h.accepts * (kExact ? 6 : 13);
+      if (getenv("STMF_GRAPH_STATS"))
+        fprintf(stderr,
+                "[stmf graph] rows %lld batches %lld esc_rounds %lld accepts %lld | sweep %.2f ms: phaseB %.2f "
+                "esc %.2f accept %.2f\n",
+                h.visits, h.batches, h.esc_rounds, h.accepts, h.sweep_ns * 1e-6, h.phaseB_ns * 1e-6,
+                h.esc_ns * 1e-6, h.acc_ns * 1e-6);
       if (h.error == 4) {
         // a direct accept changed more than kDeltaCap residuals: its numpy value from a
         // full replica of the committed state, then the sweep resumes at the next row

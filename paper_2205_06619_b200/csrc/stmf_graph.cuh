@@ -386,11 +386,25 @@ __global__ void k_g_commit(DevCtl* c, GBufs<T> B, T* __restrict__ Ut, T* __restr
   }
 }
 
-// graph-mode profiling: phase-B start time
-__global__ void k_g_tick(DevCtl* c) {
+__device__ __forceinline__ unsigned long long gtime() {
   unsigned long long now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-  c->tb0 = now;
+  return now;
+}
+
+// graph-mode profiling ticks: which = 0 phase-B start, 1 escalation round start,
+// 2 escalation round end, 3 accept body start, 4 accept body end, 5 sweep start, 6 sweep end
+__global__ void k_g_tick(DevCtl* c, int which) {
+  unsigned long long now = gtime();
+  switch (which) {
+    case 0: c->tb0 = now; break;
+    case 1: c->te0 = now; break;
+    case 2: c->esc_ns += now - c->te0; break;
+    case 3: c->ta0 = now; break;
+    case 4: c->acc_ns += now - c->ta0; break;
+    case 5: c->sweep_ns = now; break;
+    default: c->sweep_ns = now - c->sweep_ns;
+  }
 }
 
 // direct accept, replica of the committed state: residual bits |x - t1| (t1 = the
@@ -426,17 +440,23 @@ __global__ void k_res_from_product(const DevCtl* __restrict__ c, int64_t N, cons
   }
 }
 
+// direct accept with more changed entries than the delta merge takes: full sort
+// (IF h_fb1 body: CUB radix sort of slot 0, pairwise tree, k_g_fb1_fix)
+__global__ void k_g_fb1_check(const DevCtl* __restrict__ c, const double* __restrict__ out,
+                              cudaGraphConditionalHandle h_fb1) {
+  int fb = c->direct && reinterpret_cast<const long long*>(out)[1] > c->direct_cap;
+  cudaGraphSetConditional(h_fb1, fb);
+}
+__global__ void k_g_fb1_fix(const double* __restrict__ pw0, double* out) {
+  out[0] = pw0[0];
+  reinterpret_cast<long long*>(out)[1] = 0;
+}
+
 // direct accept: the replica's value becomes err (self-check: below the previous err)
-// and its arrays the current state.  More than kDeltaCap changed entries: the sweep
-// stops after this row (error 4) and the host recomputes err with a full sort.
+// and its arrays the current state
 template <typename T>
 __global__ void k_g_adopt(DevCtl* c, GBufs<T> B, int64_t N, u64* __restrict__ res_cur, u64* __restrict__ S_cur) {
   if (!c->direct) return;
-  long long D = reinterpret_cast<const long long*>(B.out)[1];
-  if (D > c->direct_cap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) c->error = 4;
-    return;
-  }
   const u64* rs = B.res[0];
   const u64* ss = B.sorted[0];
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {

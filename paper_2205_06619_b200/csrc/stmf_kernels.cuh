@@ -51,6 +51,7 @@ struct DevCtl {
   int direct_cap;        // changed-entry limit of a direct accept's delta replica
   double err_prev;       // err before a direct accept (its replica must be below)
   unsigned long long tb0, phaseB_ns;  // graph-mode phase-B timing (%globaltimer)
+  unsigned long long te0, esc_ns, ta0, acc_ns, sweep_ns;  // escalation rounds, accept bodies, whole sweep
   double sweep;          // trajectory time stamp of this sweep
   int error;             // 1: decision bound violated, 2: trajectory capacity
   int stop;              // time budget reached
