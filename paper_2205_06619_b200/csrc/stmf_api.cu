@@ -284,6 +284,9 @@ struct Session : SessionBase {
   DevBuf<T> cx, xrow_dense;
   DevBuf<T> cmi, sq;  // CM^(-i) per k for the visited row; s_q of the batch's F-ULF evals
   bool inline_ulf = getenv("STMF_INLINE") ? atoi(getenv("STMF_INLINE")) != 0 : true;
+  // phase A applies the F-URF seed itself (binary search per (eval, row)) for small m
+  bool fuse_seed = false;
+  DevBuf<SeedCols<T>> d_seedcols;
   // F-ULF hit partition of the visited row (k_hit_partition; needs the inline values)
   bool split_ulf = inline_ulf && (getenv("STMF_SPLIT") ? atoi(getenv("STMF_SPLIT")) != 0 : false);
   DevBuf<int32_t> hp_idx, hp_split;
@@ -492,6 +495,13 @@ struct Session : SessionBase {
     }
     // caches and scratch
     Ut.alloc((size_t)rank * m); V.alloc((size_t)rank * n);
+    fuse_seed = m <= 8192;
+    if (const char* e = getenv("STMF_FUSE_SEED")) fuse_seed = atoi(e) != 0;
+    if (fuse_seed) {
+      d_seedcols.alloc(1);
+      SeedCols<T> scb{col_ptr.p, row_idx.p, xc.p, Ut.p};
+      CK(cudaMemcpy(d_seedcols.p, &scb, sizeof(scb), cudaMemcpyHostToDevice));
+    }
     t1r.alloc(N); t2r.alloc(N); t1c.alloc(N); t2c.alloc(N); agr.alloc(N); agc.alloc(N);
     a2r.alloc(N); a2c.alloc(N);
     rp = (rank + (int)(16 / sizeof(T)) - 1) / (int)(16 / sizeof(T)) * (int)(16 / sizeof(T));
@@ -504,6 +514,7 @@ struct Session : SessionBase {
     ckeys.alloc(n); ckeys2.alloc(n); cvals.alloc(n); cperm.alloc(n);
     cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
     cmi.alloc((size_t)rank * n); sq.alloc(n);
+
     if (split_ulf) {
       hp_idx.alloc(N); hp_x.alloc(N); hp_t1.alloc(N); hp_t2.alloc(N); hp_ag.alloc(N); hp_split.alloc(m);
     }
@@ -968,11 +979,13 @@ struct Session : SessionBase {
     unsigned nb_ulf = nblk(G8 * n, 256), nb_urf = nblk(G8 * m, 256);
     k_phaseA<T><<<nb_ulf + nb_urf, 256, 0, st>>>(m, n, E, i, nb_ulf, bj, bk, bx, V.p, cm1.p, cm2.p, cmarg.p,
                                                  xrow_dense.p, vbuf.p, chg_ulf, sq.p, rm1.p, rm2.p, rmarg.p, ubufA.p,
-                                                 hk_dev);
+                                                 hk_dev, nullptr, nullptr, fuse_seed ? d_seedcols.p : nullptr);
     LAUNCH_CK();
-    k_phaseA_urf_seed_chk<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p,
-                                                chg_urf);
-    LAUNCH_CK();
+    if (!fuse_seed) {
+      k_phaseA_urf_seed_chk<T><<<E, 128, 0, st>>>(m, E, i, bj, bk, bx, Ut.p, col_ptr.p, row_idx.p, xc.p, ubufA.p,
+                                                  chg_urf);
+      LAUNCH_CK();
+    }
     int ng = (E + kEG - 1) / kEG;
     SideB<T> sa = side_ulf(acc_ulf, chg_ulf);
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
@@ -1393,9 +1406,11 @@ struct Session : SessionBase {
     k_g_zero<<<8, 256, 0, st>>>(c, bstate.p);
     k_phaseA<T><<<(unsigned)nsm * 4, 256, 0, st>>>(m, n, 0, 0, 0, cj.p, ck.p, cx.p, V.p, cm1.p, cm2.p, cmarg.p,
                                                    xrow_dense.p, vbuf.p, nullptr, sq.p, rm1.p, rm2.p, rmarg.p,
-                                                   ubufA.p, nullptr, c, bstate.p);
-    k_phaseA_urf_seed_chk<T><<<Emax, 128, 0, st>>>(m, 0, 0, cj.p, ck.p, cx.p, Ut.p, col_ptr.p, row_idx.p, xc.p,
-                                                    ubufA.p, nullptr, c, bstate.p);
+                                                   ubufA.p, nullptr, c, bstate.p,
+                                                   fuse_seed ? d_seedcols.p : nullptr);
+    if (!fuse_seed)
+      k_phaseA_urf_seed_chk<T><<<Emax, 128, 0, st>>>(m, 0, 0, cj.p, ck.p, cx.p, Ut.p, col_ptr.p, row_idx.p, xc.p,
+                                                      ubufA.p, nullptr, c, bstate.p);
     if (graph_prof) k_g_tick<<<1, 1, 0, st>>>(c, 0);
     {
       SideB<T> sa = side_ulf(nullptr, nullptr);

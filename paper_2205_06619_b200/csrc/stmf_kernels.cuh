@@ -753,6 +753,15 @@ __global__ void k_phaseA_urf_fill(int64_t m, int E, const int32_t* __restrict__ 
   uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
 }
 
+// what phase A needs to apply the F-URF seed column itself (small m)
+template <typename T>
+struct SeedCols {
+  const int64_t* col_ptr;
+  const int32_t* row_idx;
+  const T* xc;
+  const T* Ut;
+};
+
 // Both first residuations of a batch in one launch: blocks [0, nb_ulf) run the F-ULF
 // values (k_phaseA_ulf), the rest the F-URF fill (k_phaseA_urf_fill); block 0 also
 // copies the batch's factor indices next to the results the host reads back.
@@ -763,8 +772,10 @@ __global__ void k_phaseA(int64_t m, int64_t n, int E, int64_t i, unsigned nb_ulf
                          const T* __restrict__ xrow_dense, T* __restrict__ vI, int* __restrict__ chg_ulf,
                          T* __restrict__ s_out, const T* __restrict__ rm1, const T* __restrict__ rm2,
                          const int32_t* __restrict__ rmarg, T* __restrict__ uI, int* __restrict__ hk_out,
-                         const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr) {
+                         const DevCtl* __restrict__ g = nullptr, u64* bst = nullptr,
+                         const SeedCols<T>* __restrict__ sc = nullptr) {
   unsigned nb_total = gridDim.x;
+  int* chg_urf = nullptr;
   if (g) {  // graph mode: batch window from the control block, grid-stride over virtual blocks
     E = g->E;
     i = g->i;
@@ -772,6 +783,7 @@ __global__ void k_phaseA(int64_t m, int64_t n, int E, int64_t i, unsigned nb_ulf
     ck += g->t0;
     cx += g->t0;
     chg_ulf = reinterpret_cast<int*>(bst + 2 + 4 * (int64_t)E);
+    chg_urf = chg_ulf + E;
     int64_t G8 = (int64_t)((E + kEG - 1) / kEG) * kEG;
     nb_ulf = (unsigned)((G8 * n + 255) / 256);
     nb_total = nb_ulf + (unsigned)((G8 * m + 255) / 256);
@@ -803,7 +815,23 @@ __global__ void k_phaseA(int64_t m, int64_t n, int E, int64_t i, unsigned nb_ulf
       ilv_decode<T>(t, m, q, r);
       if (q >= E) { uI[t] = tinf<T>(); continue; }
       int64_t km = (int64_t)ck[q] * m;
-      uI[t] = (rmarg[km + r] == cj[q]) ? rm2[km + r] : rm1[km + r];
+      int j = cj[q];
+      T u = (rmarg[km + r] == j) ? rm2[km + r] : rm1[km + r];
+      if (sc) {
+        // the F-URF seed (k_phaseA_urf_seed_chk) fused: X_rj from a binary search of
+        // row r in column j, then the change flag against the current U.k
+        if (!chg_urf) chg_urf = chg_ulf + E;  // batch layout: chg = [F-ULF E][F-URF E]
+        int lo = (int)sc->col_ptr[j], hi = (int)sc->col_ptr[j + 1];
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (sc->row_idx[mid] < (int32_t)r) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < (int)sc->col_ptr[j + 1] && sc->row_idx[lo] == (int32_t)r)
+          u = vmin(u, sub_rn(sc->xc[lo], sub_rn(cx[q], sc->Ut[km + i])));
+        if (u != sc->Ut[km + r]) chg_urf[q] = 1;
+      }
+      uI[t] = u;
     }
   }
 }

@@ -116,6 +116,7 @@ def test_f32_fit_matches_restatement(monkeypatch, order, seed, m, n, r, frac, sw
     line-major runs take the host-driven loop, the group-major ones the sweep graph."""
     monkeypatch.setenv("STMF_GROUP_MAJOR", order)
     monkeypatch.setenv("STMF_GRAPH", order)
+    monkeypatch.setenv("STMF_FUSE_SEED", order)  # phase A applies the F-URF seed itself, or the seed kernel
     work, U0 = _f32_case(seed, m, n, r, frac)
     with _ext.Session(work.values, work.mask, r) as s:
         s.set_factors(U0)
