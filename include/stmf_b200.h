@@ -117,6 +117,32 @@ int stmf_objective(stmf_session* s, double* err);
 int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, double epsilon,
              double* traj_t, double* traj_err, int64_t traj_cap, int64_t* counts);
 
+/* ---- the reference's other fit methods ---- */
+
+/* families (strategies.py:60, engine.py:351-385) and ByRow selection rules (strategies.py:61) */
+enum { STMF_FAMILY_BYROW = 0, STMF_FAMILY_BYELEMENT = 1, STMF_FAMILY_BASELINE = 2, STMF_FAMILY_BYMATRIX = 3 };
+enum { STMF_SEL_TD_A = 0, STMF_SEL_TD = 1, STMF_SEL_TD_B = 2, STMF_SEL_SEQ = 3 };
+
+/*
+ * Select what stmf_run's sweep does (the strategy's sweep(run, rng), engine.py:340):
+ *   BYROW + TD_A / TD / TD_B / SEQ: byrow_sweep / byrow_seq (strategies.py:191-249);
+ *   BYELEMENT: byelement_sweep (strategies.py:252-269);
+ *   BASELINE:  _BaselineStrategy.sweep, the classic STMF (engine.py:365-380).
+ * (The caller orients the data as the strategy's orient() does.)  BYMATRIX draws
+ * a coin per candidate from the caller's RNG, so its step runs host-side over
+ * stmf_matrix_candidates + stmf_attempt; stmf_run rejects it.  The default is
+ * BYROW / TD_A (FastSTMF).  Sharded sessions support the default only.
+ */
+int stmf_set_strategy(stmf_session* s, int family, int selection);
+/* td_grid(work, U, V).sum(axis=1) of the installed factors (strategies.py:172): m doubles */
+int stmf_row_scores(stmf_session* s, double* scores);
+/*
+ * bymatrix_candidates (strategies.py:302-314): all given entries ranked by
+ * row_sum + col_sum - td (decreasing, stable in row-major order), each with its
+ * argmax k.  rows/cols/ks: N int32 each; scores: N doubles (may be NULL).
+ */
+int stmf_matrix_candidates(stmf_session* s, int32_t* rows, int32_t* cols, int32_t* ks, double* scores);
+
 /* ---- differential-test hooks (device results copied to host buffers) ---- */
 
 /* trop_matmul + argmax_grid at the given entries of the installed factors, in

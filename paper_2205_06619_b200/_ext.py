@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu"]
-HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh"]
+HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -116,6 +116,9 @@ def lib():
         "stmf_create_sim_group": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _int, _int],
         "stmf_bench_maxplus": [_i64, _i64, _int, _dbl, ctypes.c_uint64, _int, _int, _int, _vp, _vp, _vp, _vp,
                                _vp],
+        "stmf_set_strategy": [_vp, _int, _int],
+        "stmf_row_scores": [_vp, _vp],
+        "stmf_matrix_candidates": [_vp, _vp, _vp, _vp, _vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -130,7 +133,12 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
                     "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
                     "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
-                    "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus"]
+                    "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
+                    "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates"]
+
+# include/stmf_b200.h: families and ByRow selection rules
+FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
+SEL_TD_A, SEL_TD, SEL_TD_B, SEL_SEQ = 0, 1, 2, 3
 
 
 def bench_maxplus(m: int, n: int, rank: int, density: float, seed: int = 0, reps: int = 5,
@@ -337,6 +345,23 @@ class Session:
         acc = _int()
         _check(lib().stmf_attempt(self._h, op, i, j, k, ctypes.byref(f), ctypes.byref(acc)))
         return f.value, bool(acc.value)
+
+    # other fit methods -------------------------------------------------------
+    def set_strategy(self, family: int, selection: int = SEL_TD_A):
+        _check(lib().stmf_set_strategy(self._h, int(family), int(selection)))
+
+    def row_scores(self):
+        s = np.empty(self.m, np.float64)
+        _check(lib().stmf_row_scores(self._h, _p(s)))
+        return s
+
+    def matrix_candidates(self):
+        rows = np.empty(self.given, np.int32)
+        cols = np.empty(self.given, np.int32)
+        ks = np.empty(self.given, np.int32)
+        sc = np.empty(self.given, np.float64)
+        _check(lib().stmf_matrix_candidates(self._h, _p(rows), _p(cols), _p(ks), _p(sc)))
+        return rows, cols, ks, sc
 
     # measurement plumbing ----------------------------------------------------
     def stream_handle(self) -> int:

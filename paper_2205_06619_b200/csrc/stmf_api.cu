@@ -27,6 +27,7 @@
 
 #include "stmf_b200.h"
 #include "stmf_kernels.cuh"
+#include "stmf_strategies.cuh"
 #include "stmf_graph.cuh"
 
 using namespace stmf;
@@ -197,6 +198,15 @@ struct SessionBase {
   virtual void* stream() = 0;
   virtual void set_profiling(int on) = 0;
   virtual void counters(int64_t* out) = 0;
+  // the reference's other fit methods
+  virtual void set_strategy(int family, int selection) {
+    if (family != STMF_FAMILY_BYROW || selection != STMF_SEL_TD_A)
+      fail(STMF_ERR_INVALID, "sharded sessions run FastSTMF (ByRow / TD_A) only");
+  }
+  virtual void row_scores(double*) { fail(STMF_ERR_INVALID, "not available on sharded sessions"); }
+  virtual void matrix_candidates(int32_t*, int32_t*, int32_t*, double*) {
+    fail(STMF_ERR_INVALID, "not available on sharded sessions");
+  }
 };
 
 template <typename T>
@@ -512,7 +522,8 @@ struct Session : SessionBase {
     cm1.alloc((size_t)rank * n); cm2.alloc((size_t)rank * n); cmarg.alloc((size_t)rank * n);
     rm1.alloc((size_t)rank * m); rm2.alloc((size_t)rank * m); rmarg.alloc((size_t)rank * m);
     ckeys.alloc(n); ckeys2.alloc(n); cvals.alloc(n); cperm.alloc(n);
-    cj.alloc(n); ck.alloc(n); cx.alloc(n); xrow_dense.alloc(n);
+    cj.alloc(std::max<int64_t>(n, Emax)); ck.alloc(std::max<int64_t>(n, Emax));
+    cx.alloc(std::max<int64_t>(n, Emax)); xrow_dense.alloc(n);
     cmi.alloc((size_t)rank * n); sq.alloc(n);
 
     if (split_ulf) {
@@ -670,6 +681,7 @@ struct Session : SessionBase {
       }
       n_product_passes++;
       if (kExact) check_flags();
+      rscore_valid = false;
       dirty = false;
       cache_k = -1;
     }
@@ -928,8 +940,9 @@ struct Session : SessionBase {
       auto kern = nc <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
       kern<<<1, kCandThreads, 0, st>>>((int)nc, n, rank, col_idx.p + beg, xr.p + beg, agr.p + beg, score.p,
                                        colhist.p, cj.p, ck.p, cx.p, xrow_dense.p, i, cm1.p, cm2.p, cmarg.p, cmi.p,
-                                       nullptr, nullptr);
+                                       nullptr, nullptr, selection == STMF_SEL_TD ? 1 : 0);
       LAUNCH_CK();
+      cand_tdb(i, nc);
       row_partition();
       return nc;
     }
@@ -940,8 +953,10 @@ struct Session : SessionBase {
     g_cub_calls++;
     unsigned nb = std::max(1u, std::min(nblk(nc, 256), 64u));
     k_cand_build<T><<<nb, 256, sizeof(int32_t) * rank, st>>>(nc, rank, col_idx.p + beg, xr.p + beg, agr.p + beg,
-                                                             cperm.p, colhist.p, cj.p, ck.p, cx.p);
+                                                             cperm.p, colhist.p, cj.p, ck.p, cx.p,
+                                                             selection == STMF_SEL_TD ? 1 : 0);
     LAUNCH_CK();
+    cand_tdb(i, nc);
     dense_row(i);
     row_cmi(i);
     row_partition();
@@ -1039,16 +1054,21 @@ struct Session : SessionBase {
   // the first eval with f < err wins.  Returns the winner's order index or -1 and
   // commits it.  fp64: evals whose bound straddles err, and the first certain
   // accept (its numpy value becomes err), are replicated in rounds of kSlots.
-  int decide_batch(int E, const std::vector<int>& hk, double* fwin, bool* deferred = nullptr) {
+  // `order` (optional): the eval ids (2 q + op) in the strategy's attempt order; the
+  // return value is then a position in `order`.
+  int decide_batch(int E, const std::vector<int>& hk, double* fwin, bool* deferred = nullptr,
+                   const std::vector<int>* order = nullptr) {
     resolve_err();
     if (deferred) *deferred = false;
     int pos = 0;
-    while (pos < 2 * E) {
+    const int total = order ? (int)order->size() : 2 * E;
+    while (pos < total) {
       struct Req { int ev, q, op; bool certain; };
       std::vector<Req> chunk;
       int scan = pos;
-      for (; scan < 2 * E && (int)chunk.size() < (kExact ? 1 : kSlots); scan++) {
-        int q = scan >> 1, op = scan & 1;
+      for (; scan < total && (int)chunk.size() < (kExact ? 1 : kSlots); scan++) {
+        int id = order ? (*order)[scan] : scan;
+        int q = id >> 1, op = id & 1;
         if (!h_chg[op * E + q]) continue;  // state reproduced bit for bit: f == err
         double A = fx_to_double(h_acc[op * 2 * E + 2 * q + 1], h_acc[op * 2 * E + 2 * q], F);
         if (kExact) {
@@ -1167,6 +1187,8 @@ struct Session : SessionBase {
   }
 
   void row_visit(RunState& R, int64_t i) {
+    if (family == STMF_FAMILY_BYELEMENT || family == STMF_FAMILY_BASELINE) return row_visit_entries(R, i);
+    if (selection == STMF_SEL_SEQ) return row_visit_seq(R, i);
     ph_mark(-1);
     ensure_caches();
     ph_mark(0);
@@ -1218,6 +1240,264 @@ struct Session : SessionBase {
     }
     if ((int64_t)row_depth.size() == m) row_depth[i] = nc;
   }
+
+  // ---- the reference's other fit methods -------------------
+  int family = STMF_FAMILY_BYROW, selection = STMF_SEL_TD_A;
+  DevBuf<double> rscore, rs_scratch;
+  bool rscore_valid = false;
+  PWTree pwn;  // numpy pairwise tree of a length-n row (td_grid(...).sum(axis=1))
+  DevBuf<int64_t> pwn_loff;
+  DevBuf<int32_t> pwn_llen, pwn_lnode, pwn_left, pwn_right, pwn_lvloff, pwn_lvlnodes;
+  DevBuf<int64_t> cpos;
+  DevBuf<int> d_cnt;
+
+  void set_strategy(int fam, int sel) override {
+    if (fam < STMF_FAMILY_BYROW || fam > STMF_FAMILY_BYMATRIX) fail(STMF_ERR_INVALID, "unknown family %d", fam);
+    if (sel < STMF_SEL_TD_A || sel > STMF_SEL_SEQ) fail(STMF_ERR_INVALID, "unknown selection %d", sel);
+    if ((fam == STMF_FAMILY_BASELINE || sel == STMF_SEL_SEQ) && rank > Emax)
+      fail(STMF_ERR_INVALID, "rank %d exceeds the batch capacity %d", rank, Emax);
+    graph_destroy();
+    family = fam;
+    selection = sel;
+  }
+
+  // td_grid(work, U, V).sum(axis=1) of the current state (binary64: numpy's pairwise
+  // row sum bit for bit; binary32: the exact sum, like the column scores)
+  void ensure_row_scores() {
+    ensure_caches();
+    if (rscore_valid) return;
+    if (!rscore.p) rscore.alloc(m);
+    if constexpr (kExact) {
+      CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+      k_row_scores_exact<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, xr.p, t1r.p, rscore.p, exact_limit,
+                                                             flags.p);
+      LAUNCH_CK();
+      check_flags();
+    } else {
+      unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, nsm));
+      if (!pwn_loff.p) {
+        pwn.build(n);
+        upload(pwn_loff, pwn.loff); upload(pwn_llen, pwn.llen); upload(pwn_lnode, pwn.lnode);
+        upload(pwn_left, pwn.left); upload(pwn_right, pwn.right); upload(pwn_lvloff, pwn.lvl_off);
+        if (pwn.lvl_nodes.empty()) pwn.lvl_nodes.push_back(0);
+        upload(pwn_lvlnodes, pwn.lvl_nodes);
+        rs_scratch.alloc((size_t)nb * (size_t)(n + pwn.nnodes));
+      }
+      k_row_scores_pw<<<nb, 256, 0, st>>>(m, n, row_ptr.p, col_idx.p, xr.p, t1r.p, (int)pwn.loff.size(), pwn_loff.p,
+                                          pwn_llen.p, pwn_lnode.p, pwn.H, pwn_lvloff.p, pwn_lvlnodes.p, pwn_left.p,
+                                          pwn_right.p, pwn.nnodes, rs_scratch.p, rscore.p);
+      LAUNCH_CK();
+    }
+    rscore_valid = true;
+  }
+
+  void row_scores(double* out) override {
+    ensure_row_scores();
+    CK(cudaMemcpyAsync(out, rscore.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+    ssync();
+  }
+
+  // TD_B factor indices for the candidates cj[0, nc) of row i (select_k_td_b)
+  void cand_tdb(int64_t i, int64_t nc) {
+    if (selection != STMF_SEL_TD_B) return;
+    ensure_row_scores();
+    k_cand_tdb<T><<<1, 256, 0, st>>>((int)nc, rank, m, n, i, Ut.p, V.p, rscore.p, score.p, cj.p, ck.p);
+    LAUNCH_CK();
+  }
+
+  // per row visit: the dense copy of row i, CM^(-i), the hit partition
+  void row_prep(int64_t i, bool with_dense) {
+    if (with_dense) dense_row(i);
+    row_cmi(i);
+    row_partition();
+  }
+
+  // ByElement (byelement_sweep, strategies.py:252-269) and the STMF baseline
+  // (_BaselineStrategy.sweep, engine.py:365-380) visit the given entries of row i in
+  // column order and keep going after an acceptance.  Candidates from the current
+  // state are evaluated in speculative batches; the decision walks them in the
+  // reference's attempt order:
+  //   ByElement: entries with nonzero error, k = argmax, F-ULF then F-URF;
+  //   baseline:  every entry, F-ULF for k = 0..r-1, then F-URF for k = 0..r-1.
+  void row_visit_entries(RunState& R, int64_t i) {
+    const bool elem = family == STMF_FAMILY_BYELEMENT;
+    const int64_t end = h_row_ptr[i + 1];
+    const int cap = (int)std::min<int64_t>(Emax, std::max<int64_t>(n, rank));
+    if (!cpos.p) { cpos.alloc(std::max<int64_t>(n, Emax)); d_cnt.alloc(1); }
+    R.visits++;
+    ensure_caches();
+    row_prep(i, true);
+    int64_t p = h_row_ptr[i];
+    int want = std::max(1, std::min(cap, batch_floor * 2));
+    std::vector<int> hk, order;
+    std::vector<int64_t> epos;
+    while (p < end) {
+      int E = 0, ne = 0;
+      if (elem) {
+        k_cand_elem<T><<<1, 1024, 0, st>>>(p, end, want, col_idx.p, xr.p, t1r.p, agr.p, cj.p, ck.p, cx.p, cpos.p,
+                                           d_cnt.p);
+        LAUNCH_CK();
+        int cnt = 0;
+        CK(cudaMemcpyAsync(&cnt, d_cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        ssync();
+        if (cnt == 0) break;  // the rest of the row is approximated exactly
+        epos.resize(cnt);
+        CK(cudaMemcpyAsync(epos.data(), cpos.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, st));
+        E = cnt;
+      } else {
+        ne = (int)std::min<int64_t>(end - p, std::max(1, want / rank));
+        E = ne * rank;
+        k_cand_entries<T><<<nblk(E, 256), 256, 0, st>>>(p, ne, rank, col_idx.p, xr.p, cj.p, ck.p, cx.p);
+        LAUNCH_CK();
+        order.clear();
+        for (int e = 0; e < ne; e++) {
+          for (int k = 0; k < rank; k++) order.push_back(2 * (e * rank + k));
+          for (int k = 0; k < rank; k++) order.push_back(2 * (e * rank + k) + 1);
+        }
+      }
+      hk.resize(E);
+      eval_batch(i, 0, E, hk.data());
+      R.evaluated += 2 * (int64_t)E;
+      double f;
+      int w = decide_batch(E, hk, &f, nullptr, elem ? nullptr : &order);
+      if (w >= 0) {
+        R.attempts += w + 1;
+        R.accepts++;
+        err = f;
+        traj_append(R, run_now(R), err);
+        int q = (elem ? w : order[w]) >> 1;
+        p = elem ? epos[q] + 1 : p + q / rank + 1;
+        ensure_caches();
+        row_prep(i, false);
+        want = std::max(1, std::min(cap, batch_floor * 2));
+      } else {
+        R.attempts += elem ? 2 * (int64_t)E : (int64_t)order.size();
+        p = elem ? epos[E - 1] + 1 : p + ne;
+        want = std::min(cap, want * 2);
+      }
+      if (out_of_time(R)) return;
+    }
+  }
+
+  // ByRow / SEQ (byrow_seq, strategies.py:227-249): trial every (j, k, rule) of row i
+  // from the same state and keep the largest strict decrease; ties go to the smallest
+  // j, then k, then F-ULF.  binary64: every eval whose bound can reach the best is
+  // replicated (numpy's value decides); binary32: the exact objective decides.
+  void row_visit_seq(RunState& R, int64_t i) {
+    const int64_t beg = h_row_ptr[i], end = h_row_ptr[i + 1];
+    const int cap_e = (int)std::max<int64_t>(1, std::min<int64_t>(Emax, std::max<int64_t>(n, rank)) / rank);
+    R.visits++;
+    ensure_caches();
+    row_prep(i, true);
+    resolve_err();
+    struct Pot { int64_t e; int k, op; double A, mg; };
+    std::vector<Pot> pot;
+    std::vector<int> hk;
+    double best_hi = INFINITY;
+    for (int64_t p = beg; p < end;) {
+      int ne = (int)std::min<int64_t>(end - p, cap_e), E = ne * rank;
+      k_cand_entries<T><<<nblk(E, 256), 256, 0, st>>>(p, ne, rank, col_idx.p, xr.p, cj.p, ck.p, cx.p);
+      LAUNCH_CK();
+      hk.resize(E);
+      eval_batch(i, 0, E, hk.data());
+      R.evaluated += 2 * (int64_t)E;
+      for (int q = 0; q < E; q++)
+        for (int op = 0; op < 2; op++) {
+          if (!h_chg[op * E + q]) continue;  // state reproduced: f == err
+          double A = fx_to_double(h_acc[op * 2 * E + 2 * q + 1], h_acc[op * 2 * E + 2 * q], F);
+          double mg = kExact ? 0.0 : margin_of(op, A);
+          if (A - mg >= err) continue;
+          pot.push_back({p - beg + q / rank, q % rank, op, A, mg});
+          best_hi = std::min(best_hi, A + mg);
+        }
+      p += ne;
+    }
+    if (pot.empty()) return;
+    // the evals that can still be the minimum, with their objective values
+    std::vector<Pot> S;
+    for (auto& c : pot)
+      if (c.A - c.mg <= best_hi) S.push_back(c);
+    std::vector<double> fS(S.size());
+    if (kExact) {
+      for (size_t c = 0; c < S.size(); c++) fS[c] = S[c].A;
+    } else {
+      for (size_t c0 = 0; c0 < S.size(); c0 += kSlots) {
+        int cnt = (int)std::min<size_t>(kSlots, S.size() - c0);
+        set_seq_batch(i, beg, S, c0, cnt, hk);
+        for (int c = 0; c < cnt; c++) set_slot_eval(c, S[c0 + c].op, c, S[c0 + c].k);
+        replicas(cnt);
+        for (int c = 0; c < cnt; c++) fS[c0 + c] = h_pwv[c];
+      }
+    }
+    int best = -1;
+    for (size_t c = 0; c < S.size(); c++)
+      if (fS[c] < err && (best < 0 || fS[c] < fS[best])) best = (int)c;
+    if (best < 0) return;
+    // re-apply the winner (run.try_ulf / try_urf, strategies.py:245-248)
+    set_seq_batch(i, beg, S, best, 1, hk);
+    int slot = -1;
+    if (!kExact) {
+      set_slot_eval(0, S[best].op, 0, S[best].k);
+      replicas(1);
+      if (h_pwv[0] != fS[best]) fail(STMF_ERR_NUMERIC, "SEQ winner replica differs on re-evaluation");
+      slot = 0;
+    }
+    commit_eval(S[best].op, 0, S[best].k, slot);
+    err = fS[best];
+    R.attempts++;
+    R.accepts++;
+    traj_append(R, run_now(R), err);
+  }
+
+  // candidates S[c0, c0 + cnt) of row i as a batch of cnt (entry, k) candidates
+  template <typename P>
+  void set_seq_batch(int64_t i, int64_t beg, const std::vector<P>& S, size_t c0, int cnt, std::vector<int>& hk) {
+    std::vector<int32_t> hj(cnt), hkk(cnt);
+    std::vector<int64_t> hp(cnt);
+    for (int c = 0; c < cnt; c++) { hp[c] = beg + S[c0 + c].e; hkk[c] = S[c0 + c].k; }
+    for (int c = 0; c < cnt; c++) hj[c] = h_col_of(hp[c]);
+    CK(cudaMemcpyAsync(cj.p, hj.data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ck.p, hkk.data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, st));
+    for (int c = 0; c < cnt; c++) CK(cudaMemcpyAsync(cx.p + c, xr.p + hp[c], sizeof(T), cudaMemcpyDeviceToDevice, st));
+    hk.resize(cnt);
+    eval_batch(i, 0, cnt, hk.data());
+    (void)i;
+  }
+  int32_t h_col_of(int64_t p) {
+    int32_t c;
+    CK(cudaMemcpyAsync(&c, col_idx.p + p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ssync();
+    return c;
+  }
+
+  // bymatrix_step's ranked candidate list (strategies.py:281-292): every given entry
+  // (row-major order) with its argmax k and score, sorted by decreasing score (stable)
+  void matrix_candidates(int32_t* rows, int32_t* cols, int32_t* ks, double* scores) override {
+    ensure_row_scores();
+    DevBuf<u64> k1, k2;
+    DevBuf<int32_t> v1, v2, orow, ocol, ok;
+    DevBuf<double> sc, osc;
+    k1.alloc(N); k2.alloc(N); v1.alloc(N); v2.alloc(N); sc.alloc(N);
+    orow.alloc(N); ocol.alloc(N); ok.alloc(N); osc.alloc(N);
+    k_matrix_keys<T><<<nblk(N, 256), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p, rscore.p, score.p, k1.p,
+                                                     v1.p, sc.p);
+    LAUNCH_CK();
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, (int)N, 0, 64, st));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int)N, 0, 64, st));
+    g_cub_calls++;
+    k_matrix_gather<T><<<nblk(N, 256), 256, 0, st>>>(N, v2.p, rowof_r.p, col_idx.p, agr.p, sc.p, orow.p, ocol.p,
+                                                       ok.p, osc.p);
+    LAUNCH_CK();
+    CK(cudaMemcpyAsync(rows, orow.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cols, ocol.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ks, ok.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    if (scores) CK(cudaMemcpyAsync(scores, osc.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    ssync();
+  }
+
   std::vector<int64_t> row_depth;  // candidates consumed at each row's last visit
   bool rdepth_on_dev = false;      // the device copy (graph sweeps) is the current one
   void pull_row_depth() {
@@ -1260,7 +1540,8 @@ struct Session : SessionBase {
   bool graph_eligible() const {
     // rows must fit the one-block candidate ranking; column scores of a single-column
     // matrix and fixed batch schedules stay on the host loop
-    return graph_on && !fixed_sched && max_rownnz <= 4 * kCandThreads && rank <= 256 && n > 1 &&
+    return graph_on && !fixed_sched && family == STMF_FAMILY_BYROW &&
+           (selection == STMF_SEL_TD_A || selection == STMF_SEL_TD) && max_rownnz <= 4 * kCandThreads && rank <= 256 && n > 1 &&
            (kExact || cur_valid) && n_long_rows + n_long_cols == 0 && 2 * Emax <= kDecideThreads;
   }
 
@@ -1393,7 +1674,8 @@ struct Session : SessionBase {
     {
       auto kern = max_rownnz <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
       kern<<<1, kCandThreads, 0, st>>>(0, n, rank, col_idx.p, xr.p, agr.p, score.p, colhist.p, cj.p, ck.p, cx.p,
-                                       xrow_dense.p, 0, cm1.p, cm2.p, cmarg.p, cmi.p, c, row_ptr.p);
+                                       xrow_dense.p, 0, cm1.p, cm2.p, cmarg.p, cmi.p, c, row_ptr.p,
+                                       selection == STMF_SEL_TD ? 1 : 0);
     }
     row_partition();
     dr = cap_end(b_row);
@@ -1623,6 +1905,8 @@ struct Session : SessionBase {
            int64_t* counts) override {
     need_factors();
     if (budget_sweeps < 0 && !(budget_seconds > 0)) fail(STMF_ERR_INVALID, "set budget_sweeps or budget_seconds");
+    if (family == STMF_FAMILY_BYMATRIX)
+      fail(STMF_ERR_INVALID, "ByMatrix steps run host-side (stmf_matrix_candidates + stmf_attempt)");
     RunState R{};
     R.wall = budget_seconds > 0;
     R.budget_seconds = budget_seconds;
@@ -2129,6 +2413,23 @@ int stmf_attempt(stmf_session* s, int op, int64_t i, int64_t j, int k, double* f
   NEED(s);
   if (op != 0 && op != 1) return set_err(STMF_ERR_INVALID, "op must be 0 (F-ULF) or 1 (F-URF)");
   GUARD(s->impl->try_update(op, i, j, k, nullptr, nullptr, f, true, accepted));
+}
+
+int stmf_set_strategy(stmf_session* s, int family, int selection) {
+  NEED(s);
+  GUARD(s->impl->set_strategy(family, selection));
+}
+
+int stmf_row_scores(stmf_session* s, double* scores) {
+  NEED(s);
+  if (!scores) return set_err(STMF_ERR_INVALID, "null argument");
+  GUARD(s->impl->row_scores(scores));
+}
+
+int stmf_matrix_candidates(stmf_session* s, int32_t* rows, int32_t* cols, int32_t* ks, double* scores) {
+  NEED(s);
+  if (!rows || !cols || !ks) return set_err(STMF_ERR_INVALID, "null argument");
+  GUARD(s->impl->matrix_candidates(rows, cols, ks, scores));
 }
 
 int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, const void* V, void* P,

@@ -561,7 +561,7 @@ template <typename T>
 __global__ void k_cand_build(int64_t nc, int rank, const int32_t* __restrict__ cols, const T* __restrict__ xrow,
                              const uint8_t* __restrict__ agrow, const int32_t* __restrict__ perm,
                              const int32_t* __restrict__ colhist, int32_t* __restrict__ cj, int32_t* __restrict__ ck,
-                             T* __restrict__ cx) {
+                             T* __restrict__ cx, int sel = 0) {
   extern __shared__ int32_t rowhist[];
   for (int l = threadIdx.x; l < rank; l += blockDim.x) rowhist[l] = 0;
   __syncthreads();
@@ -576,6 +576,7 @@ __global__ void k_cand_build(int64_t nc, int rank, const int32_t* __restrict__ c
       int v = rowhist[l] + h[l];
       if (v > best) { best = v; k = l; }
     }
+    if (sel == 1) k = agrow[p];  // TD: argmax_k at (i, j) (strategies.py:146-148)
     cj[t] = j; ck[t] = k; cx[t] = xrow[p];
   }
 }
@@ -591,7 +592,8 @@ k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const 
            const uint8_t* __restrict__ agrow, const double* __restrict__ score, const int32_t* __restrict__ colhist,
            int32_t* __restrict__ cj, int32_t* __restrict__ ck, T* __restrict__ cx, T* __restrict__ xrow_dense,
            int64_t irow, const T* __restrict__ cm1, const T* __restrict__ cm2, const int32_t* __restrict__ cmarg,
-           T* __restrict__ cmi, const DevCtl* __restrict__ g = nullptr, const int64_t* __restrict__ row_ptr = nullptr) {
+           T* __restrict__ cmi, const DevCtl* __restrict__ g = nullptr, const int64_t* __restrict__ row_ptr = nullptr,
+           int sel = 0) {
   using Sort = cub::BlockMergeSort<u64, kCandThreads, ITEMS, int>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ int32_t rowhist[256];
@@ -638,6 +640,7 @@ k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const 
       int v = rowhist[l] + h[l];
       if (v > best) { best = v; k = l; }
     }
+    if (sel == 1) k = agrow[p];  // TD: argmax_k at (i, j) (strategies.py:146-148)
     cj[t] = j; ck[t] = k; cx[t] = xrow[p];
   }
 }

@@ -7,7 +7,7 @@ Mirrors the reference engine (engine.py) at its public names:
   * ``run_fit`` — orient (host) -> init -> device sweeps -> restore (engine.py:313-348);
   * ``f_ulf`` / ``f_urf`` — single updates computed on the device, mutating U, V in
     place and returning an ``UpdateOutcome`` (engine.py:210-237).
-Only the FastSTMF strategy runs on the device path; everything else raises.
+Every method runs on the device kernels (FastSTMF as device-resident sweep graphs).
 """
 
 from __future__ import annotations
@@ -78,17 +78,101 @@ def _orient_faststmf(R: MaskedMatrix, rng: np.random.Generator):
     return work, Orientation(transposed, row_perm, None)
 
 
+def _orient(spec, R: MaskedMatrix, rng: np.random.Generator):
+    """strategy.orient: _SpecStrategy (strategies.py:324-337) or, for the STMF
+    baseline, columns ascending by minimum without transposition (engine.py:361-363)."""
+    from .strategies import BASELINE
+    from .tropical import sort_perm_by_min
+    if spec == BASELINE:
+        perm = sort_perm_by_min(R, "cols")
+        return R.permute_cols(perm), Orientation(col_perm=perm)
+    transposed = spec.prefer_wide and R.m > R.n
+    work = R.transpose() if transposed else R.copy()
+    row_perm = col_perm = None
+    if spec.permutation == "PermR":
+        row_perm = sort_perm_by_min(work, "rows")
+        work = work.permute_rows(row_perm)
+    elif spec.permutation == "RandPermR":
+        row_perm = Permutation.random(work.m, rng)
+        work = work.permute_rows(row_perm)
+    elif spec.permutation == "PermC":
+        col_perm = sort_perm_by_min(work, "cols")
+        work = work.permute_cols(col_perm)
+    return work, Orientation(transposed, row_perm, col_perm)
+
+
+_SELECTION = {"TD_A": _ext.SEL_TD_A, "TD": _ext.SEL_TD, "TD_B": _ext.SEL_TD_B, "SEQ": _ext.SEL_SEQ}
+_FAMILY = {"ByRow": _ext.FAMILY_BYROW, "ByElement": _ext.FAMILY_BYELEMENT, "ByMatrix": _ext.FAMILY_BYMATRIX}
+
+
+def _strategy_codes(spec):
+    from .strategies import BASELINE, StrategySpec
+    if spec == BASELINE:
+        return _ext.FAMILY_BASELINE, _ext.SEL_TD_A
+    if not isinstance(spec, StrategySpec):
+        raise NotImplementedError(f"unknown strategy {spec!r}")
+    return _FAMILY[spec.family], _SELECTION[spec.selection] if spec.family == "ByRow" else _ext.SEL_TD_A
+
+
+def _run_bymatrix(s: "FitSession", config: RunConfig, rng: np.random.Generator, t0: float):
+    """run_fit's sweep loop (engine.py:328-344) with bymatrix_step (strategies.py:272-299)
+    as the sweep.  The ranked candidate list and every attempt run on the device; the
+    host only draws the reference's fair coin per candidate from the fit's RNG."""
+    wall = config.budget_seconds is not None
+    elapsed = (lambda: time.perf_counter() - t0) if wall else None
+    sweep = 0
+
+    def now():
+        return elapsed() if wall else float(sweep)
+
+    def out_of_time():
+        return wall and elapsed() >= config.budget_seconds
+
+    err = s.objective()
+    tt, te = [now()], [err]
+    attempts = accepts = sweeps = 0
+    eps = config.epsilon * err
+    if err > 0.0:
+        while True:
+            if config.budget_sweeps is not None and sweeps >= config.budget_sweeps:
+                break
+            if out_of_time():
+                break
+            sweep = sweeps + 1
+            err_before = err
+            rows, cols, ks, _ = s.matrix_candidates()
+            for d in range(rows.size):
+                if out_of_time():
+                    break
+                op = 0 if rng.random() < 0.5 else 1
+                f, accepted = s.attempt(op, int(rows[d]), int(cols[d]), int(ks[d]))
+                attempts += 1
+                if accepted:
+                    err = f
+                    accepts += 1
+                    tt.append(now())
+                    te.append(err)
+                    break
+            sweeps += 1
+            tt.append(now())
+            te.append(err)
+            if err_before - err < eps:
+                break
+    counts = {"traj_len": len(tt), "attempts": attempts, "accepts": accepts, "sweeps": sweeps,
+              "row_visits": 0, "evaluated": 2 * attempts, "replicas": 0, "product_passes": 0}
+    return np.array(tt), np.array(te), counts
+
+
 def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int | None = None):
     """Budgeted outer loop (engine.py:313-348) with the sweeps on the device.
 
-    ``strategy`` must be the FastSTMF strategy (``strategies.FASTSTMF`` or an object
-    with ``spec == FASTSTMF``); the device engine implements ByRow/TD_A only.
+    ``strategy`` is a ``StrategySpec`` (or an object with ``.spec``) or ``BASELINE``
+    ("STMF", the classic element-wise method, engine.py:351-385).  The FastSTMF
+    strategy runs its sweeps as device-resident CUDA graphs; the other methods run
+    the same device kernels under a host-driven batch loop.
     """
-    from .strategies import FASTSTMF
     spec = getattr(strategy, "spec", strategy)
-    if spec != FASTSTMF:
-        raise NotImplementedError(
-            f"the B200 engine implements FastSTMF ({FASTSTMF.name}) only, not {getattr(spec, 'name', spec)!r}")
+    family, selection = _strategy_codes(spec)
     if rank != config.rank:
         config = RunConfig(rank, config.budget_sweeps, config.budget_seconds, config.epsilon,
                            config.acol_columns, config.seed, config.audit)
@@ -97,15 +181,25 @@ def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int
     rng = np.random.default_rng(config.seed)
     wall_clock = config.budget_seconds is not None
     t0 = time.perf_counter()
-    work, orientation = _orient_faststmf(R, rng)
+    work, orientation = _orient(spec, R, rng)
     U0 = acol_means(work, rank, config.acol_columns, rng)
     with FitSession(work, rank, device) as s:
         s.set_factors(U0)
+        if (family, selection) != (_ext.FAMILY_BYROW, _ext.SEL_TD_A):
+            s.set_strategy(family, selection)
         t_init = time.perf_counter() - t0 if wall_clock else 0.0
-        budget_seconds = None
-        if wall_clock:
-            budget_seconds = max(config.budget_seconds - (time.perf_counter() - t0), 1e-9)
-        tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)
+        if family == _ext.FAMILY_BYMATRIX:
+            tt, te, counts = _run_bymatrix(s, config, rng, time.perf_counter())
+        else:
+            budget_seconds = None
+            if wall_clock:
+                budget_seconds = max(config.budget_seconds - (time.perf_counter() - t0), 1e-9)
+            # accepts per sweep: <= 1 per row visit (ByRow), <= 1 per given entry
+            # (ByElement, baseline)
+            per = work.m if family == _ext.FAMILY_BYROW else work.given_count
+            sw = config.budget_sweeps if config.budget_sweeps is not None else 64
+            tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon,
+                                   traj_cap=2 + (per + 1) * (sw + 1))
         U, V = s.get_factors()
     t_max = config.budget_seconds if wall_clock else float(config.budget_sweeps)
     traj = Trajectory(t_init=t_init, t_max=t_max, time_unit="seconds" if wall_clock else "sweeps")
@@ -139,6 +233,7 @@ def f_urf(R: MaskedMatrix, U: np.ndarray, V: np.ndarray, i: int, j: int, k: int)
     return _update(1, R, U, V, i, j, k)
 
 
-def stmf_baseline(R: MaskedMatrix, rank: int, config: RunConfig):
-    """The original element-wise STMF (engine.py:351-385) is not on the B200 path."""
-    raise NotImplementedError("STMF baseline is not implemented by the B200 engine (FastSTMF only)")
+def stmf_baseline(R: MaskedMatrix, rank: int, config: RunConfig, device: int | None = None):
+    """The original element-wise STMF (engine.py:383-385) on the device kernels."""
+    from .strategies import BASELINE
+    return run_fit(R, rank, BASELINE, config, device=device)

@@ -1,8 +1,8 @@
 """Strategy names and the public fit entry points (reference: strategies.py).
 
-``fast_stmf`` / ``fit`` keep the reference signatures.  Only the FastSTMF
-combination (ByRow, RandPermR, TD_A, wide) has a device implementation; any other
-method raises ``NotImplementedError`` — there is no CPU fallback.
+``fast_stmf`` / ``fit`` keep the reference signatures.  Every method the reference
+parses (FastSTMF, the other ByRow / ByElement / ByMatrix combinations and the STMF
+baseline) runs on the device kernels; there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -80,8 +80,6 @@ def fit(R: MaskedMatrix, rank: int, method, config: RunConfig, device: int | Non
     """Fit R with a method name or StrategySpec (strategies.py:351-357)."""
     if isinstance(method, str):
         method = parse_method(method)
-    if method == BASELINE:
-        raise NotImplementedError("STMF baseline is not implemented by the B200 engine (FastSTMF only)")
     return run_fit(R, rank, method, config, device=device)
 
 

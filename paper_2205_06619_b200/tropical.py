@@ -11,7 +11,7 @@ from . import _ext
 from .types import MaskedMatrix, Permutation
 
 __all__ = ["MaskedMatrix", "Permutation", "trop_matmul", "argmax_grid", "approx_error",
-           "masked_minplus"]
+           "masked_minplus", "sort_perm_by_min"]
 
 
 def trop_matmul(A, B) -> np.ndarray:
@@ -45,3 +45,16 @@ def masked_minplus(negU_T, R: MaskedMatrix) -> np.ndarray:
         for k in range(A.shape[0]):
             out[k] = s.residuate(0, U[:, k])
     return out
+
+
+def sort_perm_by_min(M: MaskedMatrix, axis: str) -> Permutation:
+    """Rows or columns ascending by their minimum over given entries, stable
+    (tropical.py:265-277).  Host-side: part of the strategy's orientation, which
+    runs once per fit before any device work."""
+    if axis == "rows":
+        mins = M.row_mins()
+    elif axis == "cols":
+        mins = M.col_mins()
+    else:
+        raise ValueError(f"axis must be 'rows' or 'cols', got {axis!r}")
+    return Permutation(np.argsort(mins, kind="stable"))

@@ -124,6 +124,14 @@ class MaskedMatrix:
             raise ValueError("permutation length does not match column count")
         return MaskedMatrix(self.values[:, p.forward], self.mask[:, p.forward], dtype=self.dtype)
 
+    def row_mins(self) -> np.ndarray:
+        """Per-row minimum over given entries, +inf for all-missing rows (tropical.py:141-143)."""
+        return np.min(np.where(self.mask, self.values, np.inf), axis=1)
+
+    def col_mins(self) -> np.ndarray:
+        """Per-column minimum over given entries (tropical.py:145-146)."""
+        return np.min(np.where(self.mask, self.values, np.inf), axis=0)
+
     def row_means(self) -> np.ndarray:
         """Per-row mean over given entries in float64 (reference: tropical.py:149-155)."""
         counts = self.mask.sum(axis=1)

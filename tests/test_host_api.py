@@ -15,6 +15,14 @@ from paper_2205_06619_b200 import _ext, engine, gen
 from conftest import ROOT, fit_case
 
 
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "stmf_b200.h")).read()
     return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(stmf_\w+)\s*\(", src, re.M)))
@@ -57,13 +65,16 @@ def test_parse_method():
         pkg.StrategySpec("ByElement", "TD_A", "PermC")
 
 
-def test_other_methods_fail_loudly_without_device():
+def test_every_method_needs_the_device():
+    """No CPU fallback: every fit method goes through the CUDA library."""
+    if _has_gpu():
+        pytest.skip("a CUDA device is present")
     R = pkg.MaskedMatrix(np.ones((3, 4)))
     cfg = pkg.RunConfig(rank=1, budget_sweeps=1)
-    with pytest.raises(NotImplementedError):
-        pkg.fit(R, 1, "STMF", cfg)
-    with pytest.raises(NotImplementedError):
-        pkg.fit(R, 1, "STMF_ByMatrix_NoPerm_TD_W", cfg)
+    for meth in ("STMF", "STMF_ByMatrix_NoPerm_TD_W", "STMF_ByElement_PermC_TD", "STMF_ByRow_PermR_SEQ",
+                 "FastSTMF"):
+        with pytest.raises(_ext.StmfError):
+            pkg.fit(R, 1, meth, cfg)
 
 
 def test_validation_before_device_work():
