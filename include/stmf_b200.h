@@ -162,7 +162,8 @@ int stmf_residuate(stmf_session* s, int axis, const void* vec, void* out);
 int stmf_try_update(stmf_session* s, int op, int64_t i, int64_t j, int k, void* ucol,
                     void* vrow, double* f);
 /* Same, committed when f < current error (FitRun._attempt, engine.py:278-295);
- * *accepted receives 0/1. */
+ * *accepted receives 0/1.  f is numpy's objective whenever the attempt is accepted or
+ * could be; for a certain rejection (binary64) it is the engine's bounded value. */
 int stmf_attempt(stmf_session* s, int op, int64_t i, int64_t j, int k, double* f,
                  int* accepted);
 
@@ -195,6 +196,17 @@ int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, doub
 int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps,
                        int flush_l2, int device, double* out6, float* X_out, uint32_t* mask_out,
                        float* U_out, float* V_out);
+
+/* ---- evaluation step after a fit, sessionless ---- */
+
+/* rmse(pred, truth, mask) (metrics.py:87-95): sqrt of numpy's mean of (pred - truth)**2
+ * over the masked entries (row-major), bit-identical to numpy; 0 for an empty mask.
+ * pred/truth: m x n binary64, mask: m x n bytes (nonzero = evaluated). */
+int stmf_masked_rmse(int64_t m, int64_t n, const double* pred, const double* truth, const uint8_t* mask,
+                     int device, double* out);
+/* distance_correlation(x, y) (metrics.py:98-117) of two length-len samples (len >= 2):
+ * doubly-centred distance matrices and numpy's means, bit-identical to numpy. */
+int stmf_distance_correlation(int64_t len, const double* x, const double* y, int device, double* out);
 
 /* ---- measurement plumbing ---- */
 

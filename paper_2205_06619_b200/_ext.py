@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu"]
-HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh"]
+HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh",
+           "stmf_metrics.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -58,21 +59,24 @@ def nccl_include() -> str:
     raise RuntimeError("nccl.h not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/*.cu into lib/libstmf_b200.so for sm_100a (in-tree)."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile csrc/*.cu into lib/libstmf_b200.so for sm_100a (in-tree).  ``out`` /
+    ``defines``: an experiment variant of the library (loaded with STMF_LIB)."""
+    out = out or LIB_PATH
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "stmf_b200.h")]
-    if not force and os.path.exists(LIB_PATH) and all(
-            os.path.getmtime(d) <= os.path.getmtime(LIB_PATH) for d in deps):
-        return LIB_PATH
-    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
-    tmp = LIB_PATH + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-I", nccl_include(), "-o", tmp, *srcs]
+    if not force and os.path.exists(out) and all(
+            os.path.getmtime(d) <= os.path.getmtime(out) for d in deps):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    tmp = out + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC, "-I",
+           nccl_include(), "-o", tmp, *srcs]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out)
+    return out
 
 
 _lib = None
@@ -86,10 +90,13 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise StmfError(2, f"CUDA extension not built ({LIB_PATH} missing); run "
+    # STMF_LIB: an alternative in-tree build of the same library (kernel variants
+    # compiled with other -D settings, for A/B measurements)
+    path = os.environ.get("STMF_LIB") or LIB_PATH
+    if not os.path.exists(path):
+        raise StmfError(2, f"CUDA extension not built ({path} missing); run "
                            "paper_2205_06619_b200._ext.build() — there is no CPU fallback")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     L.stmf_last_error.restype = ctypes.c_char_p
     L.stmf_version.restype = ctypes.c_char_p
     sig = {
@@ -119,6 +126,8 @@ def lib():
         "stmf_set_strategy": [_vp, _int, _int],
         "stmf_row_scores": [_vp, _vp],
         "stmf_matrix_candidates": [_vp, _vp, _vp, _vp, _vp],
+        "stmf_masked_rmse": [_i64, _i64, _vp, _vp, _vp, _int, ctypes.POINTER(_dbl)],
+        "stmf_distance_correlation": [_i64, _vp, _vp, _int, ctypes.POINTER(_dbl)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -134,7 +143,8 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
                     "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
                     "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
-                    "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates"]
+                    "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
+                    "stmf_masked_rmse", "stmf_distance_correlation"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -384,3 +394,25 @@ class Session:
         err = _dbl()
         _check(lib().stmf_bench_product(self._h, reps, int(flush_l2), ctypes.byref(ms), ctypes.byref(err)))
         return ms.value, err.value
+
+
+def masked_rmse(pred, truth, mask, device: int | None = None) -> float:
+    pred = np.ascontiguousarray(pred, dtype=np.float64)
+    truth = np.ascontiguousarray(truth, dtype=np.float64)
+    mask = np.ascontiguousarray(mask, dtype=bool)
+    if pred.shape != truth.shape or mask.shape != pred.shape or pred.ndim != 2:
+        raise ValueError("pred, truth and mask must be 2-d arrays of one shape")
+    out = _dbl()
+    dev = default_device() if device is None else device
+    _check(lib().stmf_masked_rmse(pred.shape[0], pred.shape[1], _p(pred), _p(truth), _p(mask.view(np.uint8)), dev,
+                                  ctypes.byref(out)))
+    return out.value
+
+
+def distance_correlation(x, y, device: int | None = None) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    y = np.ascontiguousarray(y, dtype=np.float64).ravel()
+    out = _dbl()
+    dev = default_device() if device is None else device
+    _check(lib().stmf_distance_correlation(x.size, _p(x), _p(y), dev, ctypes.byref(out)))
+    return out.value

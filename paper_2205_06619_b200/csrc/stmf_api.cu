@@ -28,6 +28,7 @@
 #include "stmf_b200.h"
 #include "stmf_kernels.cuh"
 #include "stmf_strategies.cuh"
+#include "stmf_metrics.cuh"
 #include "stmf_graph.cuh"
 
 using namespace stmf;
@@ -448,6 +449,7 @@ struct Session : SessionBase {
     // floor of a speculative batch (candidates): the fixed per-batch cost (~40 us of
     // launches + one host sync) ~ the cost of evaluating 8e6/N candidates
     batch_floor = (int)std::max<int64_t>(1, std::min<int64_t>(128, 8000000 / std::max<int64_t>(N, 1)));
+    if (const char* e = getenv("STMF_FLOOR")) batch_floor = std::max(1, atoi(e));
     if (batch_sched.empty()) {
       // first visit of a row: no depth history yet
       int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
@@ -1243,6 +1245,7 @@ struct Session : SessionBase {
 
   // ---- the reference's other fit methods -------------------
   int family = STMF_FAMILY_BYROW, selection = STMF_SEL_TD_A;
+  std::vector<int32_t> h_col_idx;  // host copy of the CSR column indices (try_update)
   DevBuf<double> rscore, rs_scratch;
   bool rscore_valid = false;
   PWTree pwn;  // numpy pairwise tree of a length-n row (td_grid(...).sum(axis=1))
@@ -1472,21 +1475,26 @@ struct Session : SessionBase {
 
   // bymatrix_step's ranked candidate list (strategies.py:281-292): every given entry
   // (row-major order) with its argmax k and score, sorted by decreasing score (stable)
+  DevBuf<u64> mc_k1, mc_k2;
+  DevBuf<int32_t> mc_v1, mc_v2, mc_orow, mc_ocol, mc_ok;
+  DevBuf<double> mc_sc, mc_osc;
+  DevBuf<uint8_t> mc_tmp;
   void matrix_candidates(int32_t* rows, int32_t* cols, int32_t* ks, double* scores) override {
     ensure_row_scores();
-    DevBuf<u64> k1, k2;
-    DevBuf<int32_t> v1, v2, orow, ocol, ok;
-    DevBuf<double> sc, osc;
-    k1.alloc(N); k2.alloc(N); v1.alloc(N); v2.alloc(N); sc.alloc(N);
-    orow.alloc(N); ocol.alloc(N); ok.alloc(N); osc.alloc(N);
+    auto &k1 = mc_k1, &k2 = mc_k2;
+    auto &v1 = mc_v1, &v2 = mc_v2, &orow = mc_orow, &ocol = mc_ocol, &ok = mc_ok;
+    auto &sc = mc_sc, &osc = mc_osc;
+    if (!k1.p) {
+      k1.alloc(N); k2.alloc(N); v1.alloc(N); v2.alloc(N); sc.alloc(N);
+      orow.alloc(N); ocol.alloc(N); ok.alloc(N); osc.alloc(N);
+    }
     k_matrix_keys<T><<<nblk(N, 256), 256, 0, st>>>(N, rowof_r.p, col_idx.p, xr.p, t1r.p, rscore.p, score.p, k1.p,
                                                      v1.p, sc.p);
     LAUNCH_CK();
     size_t bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, (int)N, 0, 64, st));
-    DevBuf<uint8_t> tmp;
-    tmp.alloc(bytes);
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int)N, 0, 64, st));
+    if (mc_tmp.n < bytes) mc_tmp.alloc(bytes);
+    CK(cub::DeviceRadixSort::SortPairs(mc_tmp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int)N, 0, 64, st));
     g_cub_calls++;
     k_matrix_gather<T><<<nblk(N, 256), 256, 0, st>>>(N, v2.p, rowof_r.p, col_idx.p, agr.p, sc.p, orow.p, ocol.p,
                                                        ok.p, osc.p);
@@ -1989,14 +1997,17 @@ struct Session : SessionBase {
                   int* accepted) override {
     if (i < 0 || i >= m || j < 0 || j >= n || k < 0 || k >= rank) fail(STMF_ERR_INVALID, "index out of range");
     ensure_caches();
-    // locate (i, j) among the given entries of row i (host copy of nothing: search on device)
-    int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
-    std::vector<int32_t> cols(nc);
-    CK(cudaMemcpyAsync(cols.data(), col_idx.p + beg, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
-    ssync();
-    auto it = std::lower_bound(cols.begin(), cols.end(), (int32_t)j);
-    if (it == cols.end() || *it != (int32_t)j) fail(STMF_ERR_INVALID, "entry (%lld, %lld) is missing", (long long)i, (long long)j);
-    int64_t p = beg + (it - cols.begin());
+    // locate (i, j) among the given entries of row i (host copy of the column
+    // indices, made on first use)
+    if ((int64_t)h_col_idx.size() != N) {
+      h_col_idx.resize(N);
+      CK(cudaMemcpyAsync(h_col_idx.data(), col_idx.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+      ssync();
+    }
+    auto b0 = h_col_idx.begin() + h_row_ptr[i], b1 = h_col_idx.begin() + h_row_ptr[i + 1];
+    auto it = std::lower_bound(b0, b1, (int32_t)j);
+    if (it == b1 || *it != (int32_t)j) fail(STMF_ERR_INVALID, "entry (%lld, %lld) is missing", (long long)i, (long long)j);
+    int64_t p = it - h_col_idx.begin();
     resolve_err();
     if (!err_valid) objective();
     int32_t jj = (int32_t)j, kk = k;
@@ -2014,6 +2025,15 @@ struct Session : SessionBase {
     } else if (kExact) {
       fv = fx_to_double(h_acc[op * 2 + 1], h_acc[op * 2], F);
     } else {
+      double A = fx_to_double(h_acc[op * 2 + 1], h_acc[op * 2], F);
+      if (commit_if_better && !ucol && !vrow && A - margin_of(op, A) >= err) {
+        // an attempt that certainly does not decrease the error: its objective is
+        // only reported (FitRun._attempt uses it for the decision alone), so the
+        // bounded value stands in for numpy's
+        *f = A;
+        *accepted = 0;
+        return;
+      }
       set_slot_eval(0, op, 0, k);
       replicas(1);
       fv = h_pwv[0];
@@ -2227,6 +2247,128 @@ static void trop_matmul_impl(int64_t m, int rank, int64_t n, const void* U, cons
   cudaStreamDestroy(st);
 }
 
+// ---- evaluation step: rmse, distance correlation ----------
+template <typename E>
+static void upload_vec(DevBuf<E>& d, const std::vector<E>& h, cudaStream_t st) {
+  d.alloc(std::max<size_t>(h.size(), 1));
+  if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), sizeof(E) * h.size(), cudaMemcpyHostToDevice, st));
+}
+
+// numpy's DOUBLE_pairwise_sum of a[0, len) (device array), len >= 1
+static double device_pairwise_sum(const double* a, int64_t len, cudaStream_t st) {
+  PWTree t;
+  t.build(len);
+  if (t.lvl_nodes.empty()) t.lvl_nodes.push_back(0);
+  DevBuf<int64_t> loff;
+  DevBuf<int32_t> llen, lnode, left, right, lvloff, lvlnodes;
+  upload_vec(loff, t.loff, st); upload_vec(llen, t.llen, st); upload_vec(lnode, t.lnode, st);
+  upload_vec(left, t.left, st); upload_vec(right, t.right, st); upload_vec(lvloff, t.lvl_off, st);
+  upload_vec(lvlnodes, t.lvl_nodes, st);
+  DevBuf<double> val;
+  val.alloc(t.nnodes);
+  int nl = (int)t.loff.size();
+  k_pw_leaves8<<<nblk((int64_t)nl * 8, 256), 256, 0, st>>>(nl, loff.p, llen.p, lnode.p,
+                                                          reinterpret_cast<const u64*>(a), val.p);
+  LAUNCH_CK();
+  if (t.H > 0) {
+    k_pw_combine<<<1, 1024, 0, st>>>(t.H, lvloff.p, lvlnodes.p, left.p, right.p, val.p);
+    LAUNCH_CK();
+  }
+  double r = 0;
+  CK(cudaMemcpyAsync(&r, val.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return r;
+}
+
+struct ScopedStream {
+  cudaStream_t st = nullptr;
+  explicit ScopedStream(int device) {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  }
+  ~ScopedStream() { if (st) cudaStreamDestroy(st); }
+};
+
+// rmse(pred, truth, mask) = sqrt(mean((pred - truth)[mask] ** 2)), 0 if empty (metrics.py:87-95)
+static double masked_rmse_impl(int64_t m, int64_t n, const double* pred, const double* truth, const uint8_t* mask,
+                               int device) {
+  ScopedStream S(device);
+  cudaStream_t st = S.st;
+  DevBuf<double> dp, dt, sq;
+  DevBuf<uint8_t> dm;
+  DevBuf<int64_t> rc, ptr;
+  dp.alloc((size_t)(m * n)); dt.alloc((size_t)(m * n)); dm.alloc((size_t)(m * n));
+  rc.alloc(m); ptr.alloc(m + 1);
+  CK(cudaMemcpyAsync(dp.p, pred, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dt.p, truth, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dm.p, mask, (size_t)(m * n), cudaMemcpyHostToDevice, st));
+  k_count_rows<<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dm.p, rc.p);
+  LAUNCH_CK();
+  k_scan_ptr<<<1, 1024, 0, st>>>(m, rc.p, ptr.p);
+  LAUNCH_CK();
+  int64_t N = 0;
+  CK(cudaMemcpyAsync(&N, ptr.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (N == 0) return 0.0;
+  sq.alloc(N);
+  k_masked_sqdiff<<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dp.p, dt.p, dm.p, ptr.p, sq.p);
+  LAUNCH_CK();
+  return std::sqrt(device_pairwise_sum(sq.p, N, st) / (double)N);
+}
+
+// _centered_distances(x) (metrics.py:120-123) into A (n x n)
+static void centered_distances(int64_t n, const double* dx, DevBuf<double>& A, cudaStream_t st) {
+  A.alloc((size_t)(n * n));
+  unsigned g = nblk(n * n, 256);
+  k_absdiff<<<g, 256, 0, st>>>(n, dx, A.p);
+  LAUNCH_CK();
+  DevBuf<double> cm, rm, scratch;
+  cm.alloc(n); rm.alloc(n);
+  k_colmean_seq<<<nblk(n, 128), 128, 0, st>>>(n, A.p, cm.p);
+  LAUNCH_CK();
+  PWTree t;
+  t.build(n);
+  if (t.lvl_nodes.empty()) t.lvl_nodes.push_back(0);
+  DevBuf<int64_t> loff;
+  DevBuf<int32_t> llen, lnode, left, right, lvloff, lvlnodes;
+  upload_vec(loff, t.loff, st); upload_vec(llen, t.llen, st); upload_vec(lnode, t.lnode, st);
+  upload_vec(left, t.left, st); upload_vec(right, t.right, st); upload_vec(lvloff, t.lvl_off, st);
+  upload_vec(lvlnodes, t.lvl_nodes, st);
+  unsigned nb = (unsigned)std::min<int64_t>(n, 1024);
+  scratch.alloc((size_t)nb * t.nnodes);
+  k_rowmean_pw<<<nb, 256, 0, st>>>(n, n, A.p, (int)t.loff.size(), loff.p, llen.p, lnode.p, t.H, lvloff.p, lvlnodes.p,
+                                   left.p, right.p, t.nnodes, scratch.p, rm.p);
+  LAUNCH_CK();
+  double tm = device_pairwise_sum(A.p, n * n, st) / (double)(n * n);
+  k_center<<<g, 256, 0, st>>>(n, A.p, cm.p, rm.p, tm);
+  LAUNCH_CK();
+  CK(cudaStreamSynchronize(st));
+}
+
+// distance_correlation(x, y) (metrics.py:98-117)
+static double distance_correlation_impl(int64_t n, const double* x, const double* y, int device) {
+  ScopedStream S(device);
+  cudaStream_t st = S.st;
+  DevBuf<double> dx, dy, A, B, P;
+  dx.alloc(n); dy.alloc(n);
+  CK(cudaMemcpyAsync(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dy.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  centered_distances(n, dx.p, A, st);
+  centered_distances(n, dy.p, B, st);
+  int64_t nn = n * n;
+  P.alloc((size_t)nn);
+  unsigned g = nblk(nn, 256);
+  auto mean_prod = [&](const double* a, const double* b) {
+    k_mul<<<g, 256, 0, st>>>(nn, a, b, P.p);
+    LAUNCH_CK();
+    return device_pairwise_sum(P.p, nn, st) / (double)nn;
+  };
+  double dvar_x = mean_prod(A.p, A.p), dvar_y = mean_prod(B.p, B.p);
+  if (dvar_x <= 0.0 || dvar_y <= 0.0) return 0.0;
+  double dcov2 = std::max(mean_prod(A.p, B.p), 0.0);
+  return std::sqrt(dcov2 / std::sqrt(dvar_x * dvar_y));
+}
+
 extern "C" {
 
 const char* stmf_last_error(void) { return g_err.c_str(); }
@@ -2430,6 +2572,20 @@ int stmf_matrix_candidates(stmf_session* s, int32_t* rows, int32_t* cols, int32_
   NEED(s);
   if (!rows || !cols || !ks) return set_err(STMF_ERR_INVALID, "null argument");
   GUARD(s->impl->matrix_candidates(rows, cols, ks, scores));
+}
+
+int stmf_masked_rmse(int64_t m, int64_t n, const double* pred, const double* truth, const uint8_t* mask,
+                     int device, double* out) {
+  if (!pred || !truth || !mask || !out) return set_err(STMF_ERR_INVALID, "null argument");
+  if (m < 0 || n < 0) return set_err(STMF_ERR_INVALID, "bad shape");
+  if (m == 0 || n == 0) { *out = 0.0; return STMF_OK; }
+  GUARD(*out = masked_rmse_impl(m, n, pred, truth, mask, device));
+}
+
+int stmf_distance_correlation(int64_t len, const double* x, const double* y, int device, double* out) {
+  if (!x || !y || !out) return set_err(STMF_ERR_INVALID, "null argument");
+  if (len < 2) return set_err(STMF_ERR_INVALID, "need at least two samples");
+  GUARD(*out = distance_correlation_impl(len, x, y, device));
 }
 
 int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, const void* V, void* P,

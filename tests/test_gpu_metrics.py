@@ -1,0 +1,75 @@
+"""Device evaluation step: prediction rmse and (masked)
+distance correlation, bit-identical to the reference's numpy expressions
+(metrics.py:87-139, restated here as the checker)."""
+
+import numpy as np
+import pytest
+
+import paper_2205_06619_b200 as pkg
+from paper_2205_06619_b200 import metrics
+
+pytestmark = pytest.mark.gpu
+
+
+def np_rmse(pred, truth, mask):  # metrics.py:87-95
+    diff = (np.asarray(pred, np.float64) - np.asarray(truth, np.float64))[np.asarray(mask, bool)]
+    return 0.0 if diff.size == 0 else float(np.sqrt(np.mean(diff ** 2)))
+
+
+def np_cd(x):  # metrics.py:120-123
+    d = np.abs(x[:, None] - x[None, :])
+    return d - d.mean(axis=0)[None, :] - d.mean(axis=1)[:, None] + d.mean()
+
+
+def np_dc(x, y):  # metrics.py:98-117
+    A, B = np_cd(np.asarray(x, np.float64).ravel()), np_cd(np.asarray(y, np.float64).ravel())
+    dvx, dvy = np.mean(A * A), np.mean(B * B)
+    if dvx <= 0.0 or dvy <= 0.0:
+        return 0.0
+    return float(np.sqrt(max(np.mean(A * B), 0.0) / np.sqrt(dvx * dvy)))
+
+
+def test_rmse_matches_numpy():
+    rng = np.random.default_rng(1)
+    for m, n, d in ((1, 1, 1.0), (7, 13, 0.5), (100, 200, 0.2), (300, 1000, 0.9), (64, 64, 0.0)):
+        pred = rng.normal(size=(m, n))
+        truth = rng.normal(size=(m, n)) * 3
+        mask = rng.random((m, n)) < d
+        assert metrics.rmse(pred, truth, mask) == np_rmse(pred, truth, mask), (m, n, d)
+
+
+def test_prediction_rmse_of_a_fit():
+    """The reference's evaluation flow: fit on the training mask, rmse of
+    FactorPair.product() on the held-out entries."""
+    from paper_2205_06619_b200 import gen
+    R = gen.config1()
+    full = np.where(R.mask, R.values, 0.0)
+    rng = np.random.default_rng(4)
+    test = R.mask & (rng.random(R.mask.shape) < 0.1)
+    train = pkg.MaskedMatrix(R.values, R.mask & ~test)
+    pair, _ = pkg.fast_stmf(train, 3, pkg.RunConfig(rank=3, budget_sweeps=2, epsilon=0.0, seed=42))
+    P = pair.product()
+    assert np.array_equal(P, np.max(pair.U[:, :, None] + pair.V[None, :, :], axis=1))
+    assert metrics.rmse(P, full, test) == np_rmse(P, full, test)
+
+
+def test_distance_correlation_matches_numpy():
+    rng = np.random.default_rng(2)
+    for n in (2, 3, 17, 129, 500, 2000):
+        x = rng.normal(size=n)
+        y = x * 0.5 + rng.normal(size=n) * 0.3
+        assert metrics.distance_correlation(x, y) == np_dc(x, y), n
+    assert metrics.distance_correlation(np.ones(5), np.arange(5.0)) == 0.0
+    with pytest.raises(ValueError):
+        metrics.distance_correlation([1.0], [2.0])
+
+
+def test_masked_dc_subsamples_like_the_reference():
+    rng = np.random.default_rng(3)
+    truth = rng.normal(size=(80, 60))
+    approx = truth + rng.normal(size=(80, 60)) * 0.2
+    mask = rng.random((80, 60)) < 0.7
+    x, y = truth[mask], approx[mask]
+    idx = np.random.default_rng(0).choice(x.size, size=2000, replace=False)
+    assert metrics.masked_dc(truth, approx, mask) == np_dc(x[idx], y[idx])
+    assert metrics.masked_dc(truth, approx, mask, max_entries=10_000) == np_dc(x, y)
