@@ -208,6 +208,17 @@ int stmf_masked_rmse(int64_t m, int64_t n, const double* pred, const double* tru
  * doubly-centred distance matrices and numpy's means, bit-identical to numpy. */
 int stmf_distance_correlation(int64_t len, const double* x, const double* y, int device, double* out);
 
+/* ---- data input, host-side ---- */
+
+/* load_matrix_csv (io.py:33-60): open (reads and indexes the file, reports the
+ * shape), fill the values (m x n binary64, NaN where missing) and the given-mask
+ * (m x n bytes) on `threads` host threads (<= 0: all), close.  "" and "nan" (any
+ * case) are missing; blank records are skipped; has_header skips the first record;
+ * ragged rows and unparsable cells are STMF_ERR_INVALID (message as the reference's). */
+int stmf_csv_open(const char* path, int has_header, void** handle, int64_t* m, int64_t* n);
+int stmf_csv_fill(void* handle, double* values, uint8_t* mask, int threads);
+int stmf_csv_close(void* handle);
+
 /* ---- measurement plumbing ---- */
 
 /* The session's cudaStream_t (all device work of the session is ordered on it). */

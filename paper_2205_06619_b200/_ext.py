@@ -18,7 +18,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "lib", "libstmf_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
-SOURCES = ["stmf_api.cu"]
+SOURCES = ["stmf_api.cu", "stmf_io.cc"]
 HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh",
            "stmf_metrics.cuh"]
 
@@ -128,6 +128,9 @@ def lib():
         "stmf_matrix_candidates": [_vp, _vp, _vp, _vp, _vp],
         "stmf_masked_rmse": [_i64, _i64, _vp, _vp, _vp, _int, ctypes.POINTER(_dbl)],
         "stmf_distance_correlation": [_i64, _vp, _vp, _int, ctypes.POINTER(_dbl)],
+        "stmf_csv_open": [ctypes.c_char_p, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+        "stmf_csv_fill": [_vp, _vp, _vp, _int],
+        "stmf_csv_close": [_vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -144,7 +147,8 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
                     "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
-                    "stmf_masked_rmse", "stmf_distance_correlation"]
+                    "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
+                    "stmf_csv_close"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -416,3 +420,17 @@ def distance_correlation(x, y, device: int | None = None) -> float:
     dev = default_device() if device is None else device
     _check(lib().stmf_distance_correlation(x.size, _p(x), _p(y), dev, ctypes.byref(out)))
     return out.value
+
+
+def csv_read(path: str, has_header: bool = False, threads: int = 0):
+    """Native load_matrix_csv: (values float64 with NaN where missing, mask bool)."""
+    m, n, h = _i64(), _i64(), _vp()
+    _check(lib().stmf_csv_open(os.fsencode(path), int(has_header), ctypes.byref(h), ctypes.byref(m),
+                               ctypes.byref(n)))
+    try:
+        values = np.empty((m.value, n.value), np.float64)
+        mask = np.empty((m.value, n.value), np.uint8)
+        _check(lib().stmf_csv_fill(h, _p(values), _p(mask), int(threads)))
+    finally:
+        lib().stmf_csv_close(h)
+    return values, mask.view(bool)

@@ -47,6 +47,9 @@ static int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+// error reporting for the host-only sources (stmf_io.cc)
+int stmf_io_set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+
 struct StmfError {
   int code;
 };

@@ -1,0 +1,90 @@
+"""Matrix input/output, CPU only: the native CSV reader
+against the reference's parsing rules (io.py:33-60, restated below as the checker),
+the writer's round trip, and the binary masked-matrix format."""
+
+import csv
+
+import numpy as np
+import pytest
+
+import paper_2205_06619_b200 as pkg
+from paper_2205_06619_b200 import io as sio
+
+
+def ref_load(path, has_header=False):
+    """io.py:33-60: csv records, blank records skipped, cells stripped, "" / "nan" missing."""
+    rows, masks = [], []
+    with open(path, newline="") as fh:
+        for idx, record in enumerate(csv.reader(fh)):
+            if has_header and idx == 0:
+                continue
+            if not record:
+                continue
+            vals, given = [], []
+            for cell in record:
+                tok = cell.strip()
+                if tok.lower() in {"", "nan"}:
+                    vals.append(np.nan)
+                    given.append(False)
+                else:
+                    vals.append(float(tok))
+                    given.append(True)
+            rows.append(vals)
+            masks.append(given)
+    if not rows:
+        raise ValueError(f"{path}: no data rows")
+    widths = {len(r) for r in rows}
+    if len(widths) != 1:
+        raise ValueError(f"{path}: ragged rows (widths {sorted(widths)})")
+    return np.array(rows), np.array(masks)
+
+
+def same(R, ref):
+    vals, mask = ref
+    return np.array_equal(R.mask, mask) and np.array_equal(R.values[mask], vals[mask])
+
+
+def test_roundtrip_random(tmp_path):
+    rng = np.random.default_rng(0)
+    for t, (m, n) in enumerate([(1, 1), (5, 7), (40, 33), (300, 120)]):
+        X = rng.normal(size=(m, n)) * 10.0 ** rng.integers(-8, 9, size=(m, n))
+        M = rng.random((m, n)) < 0.7
+        M[:, 0] = True
+        M[0, :] = True
+        R = pkg.MaskedMatrix(X, M)
+        p = tmp_path / f"r{t}.csv"
+        sio.save_matrix_csv(p, R, header=[f"c{j}" for j in range(n)] if t % 2 else None)
+        L = sio.load_matrix_csv(p, has_header=bool(t % 2), threads=3)
+        assert same(L, ref_load(p, bool(t % 2)))
+        assert np.array_equal(L.values[M], X[M]) and np.array_equal(L.mask, M)
+
+
+def test_reference_parsing_rules(tmp_path):
+    text = 'h1,h2,h3\r\n 1.5 ,nan,\n\n"2.25",NaN,  -3e-5\n1_000,  ,7\n'
+    p = tmp_path / "rules.csv"
+    p.write_text(text)
+    L = sio.load_matrix_csv(p, has_header=True)
+    assert same(L, ref_load(p, True))
+    assert L.shape == (3, 3)
+
+
+@pytest.mark.parametrize("text,msg", [("1,2\n3\n", "ragged rows"), ("\n\n", "no data rows"),
+                                      ("1,abc\n", "could not convert")])
+def test_errors(tmp_path, text, msg):
+    p = tmp_path / "bad.csv"
+    p.write_text(text)
+    with pytest.raises(ValueError, match=msg):
+        ref_load(p)
+    with pytest.raises(ValueError, match=msg):
+        sio.load_matrix_csv(p)
+
+
+def test_binary_format(tmp_path):
+    from paper_2205_06619_b200 import gen
+    for R in (gen.config1(), gen.config3(m=64, n=96, rank=3)):
+        p = tmp_path / "m.bin"
+        sio.save_matrix_bin(p, R)
+        L = sio.load_matrix_bin(p)
+        assert L.dtype == R.dtype and np.array_equal(L.mask, R.mask)
+        assert np.array_equal(L.values[R.mask], R.values[R.mask])
+        assert p.stat().st_size == 32 + (R.m * R.n + 7) // 8 + R.given_count * R.values.itemsize
