@@ -1,5 +1,6 @@
+"""Diagnostics: one wall-clock-budgeted run after warm sweeps, for ncu captures (python tools/diag_budget_run.py CONFIG SECONDS WARM)."""
 import sys, time, numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2205_06619_b200 import gen, engine, _ext
 cfgno = int(sys.argv[1]); secs = float(sys.argv[2]); warm = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 C = gen.CONFIGS[cfgno]

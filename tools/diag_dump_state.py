@@ -1,5 +1,6 @@
+"""Diagnostics: dump the work-orientation data and factors after N sweeps to gpurun_out/state_cN.npz."""
 import sys, numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2205_06619_b200 import gen, engine, _ext
 cfg = int(sys.argv[1]); sweeps = float(sys.argv[2])
 C = gen.CONFIGS[cfg]; R = C["make"]()

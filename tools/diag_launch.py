@@ -1,5 +1,6 @@
+"""Diagnostics: launch-count / timing probe of one fit (kept from round-1 investigations)."""
 import sys, numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2205_06619_b200 import gen, engine, _ext
 cfg = int(sys.argv[1]); warm = int(sys.argv[2]); secs = float(sys.argv[3]) if len(sys.argv) > 3 else 0
 C = gen.CONFIGS[cfg]; R = C["make"]()

@@ -1,5 +1,6 @@
+"""Diagnostics: per-sweep wall times of the device engine on a config (python tools/diag_sweep_times.py CONFIG SWEEPS)."""
 import sys, time, numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_2205_06619_b200 as pkg
 from paper_2205_06619_b200 import gen, engine, _ext
 cfgno = int(sys.argv[1]) if len(sys.argv) > 1 else 2
