@@ -22,6 +22,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -213,26 +215,96 @@ struct SessionBase {
   }
 };
 
+// Device buffers come from the device's stream-ordered memory pool, which keeps freed
+// memory mapped (release threshold = max): creating and destroying a session then
+// costs pool bookkeeping instead of ~140 cudaMalloc / cudaFree calls, whose page
+// mapping work measured 15-1000 ms per fit on the GPU box (tools/diag_e2e_parts.py).
+// Allocation is ordered on the legacy stream and completed before use; a free first
+// waits for the device (no kernel can still be using the buffer), then returns the
+// block to the pool.
+static void pool_setup(int dev) {
+  static bool done[64] = {false};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+static void* dev_alloc(size_t bytes) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  pool_setup(dev);
+  void* p = nullptr;
+  CK(cudaMallocAsync(&p, bytes, 0));
+  CK(cudaStreamSynchronize(0));
+  return p;
+}
+
+static void dev_free(void* p, int dev) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, 0);
+  if (cur != dev) cudaSetDevice(cur);
+}
+
+// Pinned host staging buffers (per-batch decision data, control blocks) are cached
+// process-wide by size: page-locking is a slow driver call, and a fit's session
+// needs a handful of small ones.
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void*> g_pin_free;
+template <typename P>
+static void pinned_alloc(P** out, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.find(bytes);
+    if (it != g_pin_free.end()) {
+      *out = static_cast<P*>(it->second);
+      g_pin_free.erase(it);
+      return;
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMallocHost(&p, bytes));
+  *out = static_cast<P*>(p);
+}
+static void pinned_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace(bytes, p);
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   bool own = true;
-  void alloc(size_t cnt) {
-    if (p && own) cudaFree(p);
+  int dev = 0;
+  void release() {
+    if (p && own) dev_free(p, dev);
     p = nullptr;
+  }
+  void alloc(size_t cnt) {
+    release();
     own = true;
     n = cnt;
-    if (cnt) CK(cudaMalloc(&p, cnt * sizeof(T)));
+    if (cnt) {
+      CK(cudaGetDevice(&dev));
+      p = static_cast<T*>(dev_alloc(cnt * sizeof(T)));
+    }
   }
   // a non-owning view into another allocation
   void view(T* ptr, size_t cnt) {
-    if (p && own) cudaFree(p);
+    release();
     p = ptr;
     n = cnt;
     own = false;
   }
-  ~DevBuf() { if (p && own) cudaFree(p); }
+  ~DevBuf() { release(); }
 };
 
 template <typename T>
@@ -384,14 +456,14 @@ struct Session : SessionBase {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
-    if (h_ctl) cudaFreeHost(h_ctl);
+    pinned_free(h_ctl, sizeof(DevCtl));
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
-    if (h_bstate) cudaFreeHost(h_bstate);
-    if (h_dcount) cudaFreeHost(h_dcount);
-    if (h_out) cudaFreeHost(h_out);
-    if (h_pwv) cudaFreeHost(h_pwv);
-    if (h_flags) cudaFreeHost(h_flags);
+    pinned_free(h_bstate, sizeof(u64) * bstate.n);
+    pinned_free(h_dcount, sizeof(int) * kSlots);
+    pinned_free(h_out, sizeof(double) * 2 * kSlots);
+    pinned_free(h_pwv, sizeof(double) * kSlots);
+    pinned_free(h_flags, sizeof(int) * 4);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -544,10 +616,10 @@ struct Session : SessionBase {
     acc.view(bstate.p + 2, 4 * (size_t)Emax);
     chg.view(reinterpret_cast<int*>(bstate.p + 2 + 4 * (size_t)Emax), 2 * (size_t)Emax);
     findpos.alloc(2);
-    CK(cudaMallocHost(&h_bstate, sizeof(u64) * bstate.n));
+    pinned_alloc(&h_bstate, sizeof(u64) * bstate.n);
     h_acc = h_bstate + 2;
     h_chg = reinterpret_cast<int*>(h_bstate + 2 + 4 * (size_t)Emax);
-    CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
+    pinned_alloc(&h_flags, sizeof(int) * 4);
     h_flags[0] = h_flags[1] = 0;
     size_t b1 = 0, b2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ckeys.p, ckeys2.p, cvals.p, cperm.p, (int)n, 0, 64, st));
@@ -750,7 +822,7 @@ struct Session : SessionBase {
 
   void alloc_slots() {
     static_assert(kSlots == kRepSlots, "replica round size");
-    CK(cudaMallocHost(&h_out, sizeof(double) * 2 * kSlots));
+    pinned_alloc(&h_out, sizeof(double) * 2 * kSlots);
     d_dcounts.alloc(kSlots);
     CK(cudaMemset(d_dcounts.p, 0, sizeof(int) * kSlots));
     d_pwout.alloc(2 * kSlots);
@@ -759,8 +831,8 @@ struct Session : SessionBase {
       s.res.alloc(N); s.sorted.alloc(N); s.olds.alloc(kDeltaCap); s.news.alloc(kDeltaCap); s.dcount.alloc(1);
       s.a.alloc(m); s.b.alloc(n); s.pw.alloc(pw.nnodes);
     }
-    CK(cudaMallocHost(&h_dcount, sizeof(int) * kSlots));
-    CK(cudaMallocHost(&h_pwv, sizeof(double) * kSlots));
+    pinned_alloc(&h_dcount, sizeof(int) * kSlots);
+    pinned_alloc(&h_pwv, sizeof(double) * kSlots);
   }
 
   void pw_sum(Slot& s) {
@@ -1644,7 +1716,7 @@ struct Session : SessionBase {
     }
     if (!dctl.p) {
       dctl.alloc(1);
-      CK(cudaMallocHost(&h_ctl, sizeof(DevCtl)));
+      pinned_alloc(&h_ctl, sizeof(DevCtl));
       d_row_depth.alloc(m);
       d_traj_t.alloc(m + 1);
       d_traj_e.alloc(m + 1);
@@ -2498,8 +2570,10 @@ int stmf_create_sim_group(stmf_session** out, int dtype, int64_t m, int64_t n, i
 
 int stmf_destroy(stmf_session* s) {
   if (!s) return STMF_OK;
+  double t0 = now_s();
   delete s->impl;
   delete s;
+  if (getenv("STMF_TRACE_TEARDOWN")) fprintf(stderr, "[stmf teardown] total %.2f ms\n", (now_s() - t0) * 1e3);
   return STMF_OK;
 }
 

@@ -342,10 +342,10 @@ struct ShardGroup : SessionBase {
   int gridX = -1000;
 
   ~ShardGroup() override {
-    if (h_acc) cudaFreeHost(h_acc);
-    if (h_limbs) cudaFreeHost(h_limbs);
-    if (h_chg) cudaFreeHost(h_chg);
-    if (h_flags) cudaFreeHost(h_flags);
+    pinned_free(h_acc, sizeof(u64) * 4 * Emax);
+    pinned_free(h_limbs, sizeof(int64_t) * 6 * Emax);
+    pinned_free(h_chg, sizeof(int) * 2 * Emax);
+    pinned_free(h_flags, sizeof(int) * 4);
     sh.clear();
     comm.reset();
     if (st) cudaStreamDestroy(st);
@@ -405,10 +405,10 @@ struct ShardGroup : SessionBase {
       Mp += s->ml * n;
       sh.push_back(std::move(s));
     }
-    CK(cudaMallocHost(&h_acc, sizeof(u64) * 4 * Emax));
-    CK(cudaMallocHost(&h_limbs, sizeof(int64_t) * 6 * Emax));
-    CK(cudaMallocHost(&h_chg, sizeof(int) * 2 * Emax));
-    CK(cudaMallocHost(&h_flags, sizeof(int) * 4));
+    pinned_alloc(&h_acc, sizeof(u64) * 4 * Emax);
+    pinned_alloc(&h_limbs, sizeof(int64_t) * 6 * Emax);
+    pinned_alloc(&h_chg, sizeof(int) * 2 * Emax);
+    pinned_alloc(&h_flags, sizeof(int) * 4);
     {
       double nl = 0;
       for (auto& s : sh) nl += (double)s->Nl;
