@@ -292,15 +292,35 @@ def run_b200(args):
             traffic, traffic_src = tr["bytes"], tr["capture"]
     except (OSError, ValueError):
         pass
+    # the binding resource is instruction issue (profiles/r01_v4_phaseB.md): warp
+    # instructions per (entry, evaluation) from the committed ncu capture, times the
+    # live (entry, evaluation) rate, against the issue peak of the SMs
+    issue = None
+    try:
+        ti = json.load(open(os.path.join(ROOT, "profiles", "r01_phaseB_traffic.json"))).get(str(args.config), {})
+        ti = ti.get("issue")
+        if ti and nb:
+            ipe = ti["warp_instructions"] / (ti["evals"] * ti["given"])
+            rate = evals_per_launch * N / avg_s
+            prop = torch.cuda.get_device_properties(local)
+            sm_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+            ipeak = prop.multi_processor_count * 4 * sm_hz
+            issue = {"warp_inst_per_entry_eval": ipe, "entry_evals_per_s": rate,
+                     "achieved_warp_inst_per_s": ipe * rate, "peak_warp_inst_per_s": ipeak,
+                     "frac": ipe * rate / ipeak, "source": ti["capture"]}
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "stmf::k_phaseB (candidate evaluation: 2nd residuation + error, both rules)",
                 "bytes_per_launch": b_launch, "bytes_per_attempt": 2 * b_pass,
                 "evals_per_launch": evals_per_launch, "avg_launch_us": avg_s * 1e6, "launches": nb,
                 "share_of_step": (b_ns / 1e9) / t_dev if t_dev else None, "peak_source": peak_src,
+                "issue": issue,
                 "note": ("one pass over the given entries serves a group of 8 evaluations and the working "
-                         "set is L2-resident, so the HBM-equivalent rate can exceed the HBM peak; the kernel "
-                         "is issue-bound on fp64 compare/select (DESIGN.md, profiles/)") if l2_resident else
+                         "set is L2-resident, so the HBM-equivalent rate can exceed the HBM peak; the binding "
+                         "resource is instruction issue (roofline.issue; DESIGN.md, profiles/r01_v4_phaseB.md)")
+                        if l2_resident else
                         "one pass over the given entries serves a group of 8 evaluations (DESIGN.md)"}
 
     line = None
