@@ -456,6 +456,9 @@ struct Session : SessionBase {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
+    if (ev_fork3) cudaEventDestroy(ev_fork3);
+    if (ev_join3) cudaEventDestroy(ev_join3);
+    if (st3) cudaStreamDestroy(st3);
     pinned_free(h_ctl, sizeof(DevCtl));
     if (ev_b0) cudaEventDestroy(ev_b0);
     if (ev_b1) cudaEventDestroy(ev_b1);
@@ -1667,6 +1670,8 @@ struct Session : SessionBase {
 
   cudaStream_t st2 = nullptr;          // second capture stream (graph branches)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st3 = nullptr;          // third capture stream (residuation statistics after an accept)
+  cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
   // pairwise-tree combine of a replica round read from the device descriptor
   void launch_combine(int ys, RepRound<T>* rp_, cudaStream_t s_) {
     RepRound<T> none{};
@@ -1713,6 +1718,9 @@ struct Session : SessionBase {
       CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      CK(cudaStreamCreateWithFlags(&st3, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork3, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join3, cudaEventDisableTiming));
     }
     if (!dctl.p) {
       dctl.alloc(1);
@@ -1841,6 +1849,15 @@ struct Session : SessionBase {
                                         kExact ? nullptr : S_cur.p);
       unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
       const int* kc = &c->cache_k;
+      // the residuation statistics of index k need only the committed factors: a
+      // third branch, overlapped with the product caches and the column scores
+      CK(cudaEventRecord(ev_fork3, st));
+      CK(cudaStreamWaitEvent(st3, ev_fork3, 0));
+      k_line_stats<T><<<warps_grid(n), 256, 0, st3>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p, cm1.p, cm2.p, cmarg.p, 0,
+                                                         kc, m, n);
+      k_line_stats<T><<<warps_grid(m), 256, 0, st3>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
+                                                         kc, n, m);
+      CK(cudaEventRecord(ev_join3, st3));
       k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
                                            t1r.p, t2r.p, agr.p, a2r.p, kc);
       if (!kExact) {
@@ -1865,10 +1882,7 @@ struct Session : SessionBase {
                                            t1c.p, t2c.p, agc.p, a2c.p, kc);
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
                                                    !kExact, exact_limit, flags.p);
-      k_line_stats<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p, cm1.p, cm2.p, cmarg.p, 0,
-                                                        kc, m, n);
-      k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
-                                                        kc, n, m);
+      CK(cudaStreamWaitEvent(st, ev_join3, 0));
       if (!kExact) CK(cudaStreamWaitEvent(st, ev_join, 0));
       da = cap_end(b_acc);
       if (!kExact) {
