@@ -199,3 +199,26 @@ def test_attempt_commit_semantics(fits):
         U, V = s.get_factors()
     with session(X, M, U, V) as s2:
         assert s2.objective() == e0  # committed error == fresh objective of the state
+
+
+def test_config2_distribution_crop_matches_reference():
+    """binary64 path on config 2's data distribution (log2(1 + lognormal), 50% missing,
+    rank 5): a 200 x 400 crop, 5 sweeps, against the unmodified reference's fit
+    (tests/golden/c2crop.npz, make_golden_c2crop.py) — factors and trajectory bit for bit,
+    through the sweep graph and through the host-driven loop."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c2crop.npz")
+    if not os.path.exists(path):
+        pytest.skip("c2crop fixture not generated")
+    g = np.load(path)
+    R = pkg.MaskedMatrix(g["R"], g["M"])
+    cfg = pkg.RunConfig(rank=int(g["rank"]), budget_sweeps=int(g["sweeps"]), epsilon=0.0, seed=int(g["seed"]))
+    for graph in ("1", "0"):
+        os.environ["STMF_GRAPH"] = graph
+        try:
+            pair, traj = pkg.fast_stmf(R, int(g["rank"]), cfg)
+        finally:
+            os.environ.pop("STMF_GRAPH", None)
+        assert np.array_equal(np.array(traj.errors), g["traj_e"]), graph
+        assert np.array_equal(np.array(traj.times), g["traj_t"]), graph
+        assert np.array_equal(pair.U, g["U"]) and np.array_equal(pair.V, g["V"]), graph
