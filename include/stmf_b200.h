@@ -219,6 +219,13 @@ int stmf_csv_open(const char* path, int has_header, void** handle, int64_t* m, i
 int stmf_csv_fill(void* handle, double* values, uint8_t* mask, int threads);
 int stmf_csv_close(void* handle);
 
+/* ---- memory ---- */
+
+/* Device buffers of sessions come from the device's stream-ordered memory pool, which
+ * keeps freed blocks for the next session (setup and teardown then cost no page
+ * mapping).  This returns the unused blocks of `device` to the driver. */
+int stmf_release_memory(int device);
+
 /* ---- measurement plumbing ---- */
 
 /* The session's cudaStream_t (all device work of the session is ordered on it). */

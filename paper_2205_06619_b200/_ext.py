@@ -131,6 +131,7 @@ def lib():
         "stmf_csv_open": [ctypes.c_char_p, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
         "stmf_csv_fill": [_vp, _vp, _vp, _int],
         "stmf_csv_close": [_vp],
+        "stmf_release_memory": [_int],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -148,7 +149,7 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
-                    "stmf_csv_close"]
+                    "stmf_csv_close", "stmf_release_memory"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -434,3 +435,8 @@ def csv_read(path: str, has_header: bool = False, threads: int = 0):
     finally:
         lib().stmf_csv_close(h)
     return values, mask.view(bool)
+
+
+def release_memory(device: int | None = None):
+    """Return the device memory pool's unused blocks (kept for reuse by later sessions)."""
+    _check(lib().stmf_release_memory(default_device() if device is None else device))

@@ -2679,6 +2679,16 @@ int stmf_distance_correlation(int64_t len, const double* x, const double* y, int
   GUARD(*out = distance_correlation_impl(len, x, y, device));
 }
 
+int stmf_release_memory(int device) {
+  GUARD({
+    cudaMemPool_t pool;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    CK(cudaMemPoolTrimTo(pool, 0));
+  });
+}
+
 int stmf_trop_matmul(int dtype, int64_t m, int rank, int64_t n, const void* U, const void* V, void* P,
                      int32_t* arg, int device) {
   if (!U || !V) return set_err(STMF_ERR_INVALID, "null argument");

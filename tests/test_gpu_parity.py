@@ -222,3 +222,16 @@ def test_config2_distribution_crop_matches_reference():
         assert np.array_equal(np.array(traj.errors), g["traj_e"]), graph
         assert np.array_equal(np.array(traj.times), g["traj_t"]), graph
         assert np.array_equal(pair.U, g["U"]) and np.array_equal(pair.V, g["V"]), graph
+
+
+def test_pooled_memory_release_between_fits(fits):
+    """Session buffers come from the device memory pool; releasing it between fits
+    changes nothing in the results."""
+    c = fit_case(fits, "s2")
+    R = pkg.MaskedMatrix(c["R"], c["M"])
+    cfg = pkg.RunConfig(rank=int(c["rank"]), budget_sweeps=int(c["sweeps"]), epsilon=0.0, seed=int(c["seed"]))
+    p1, t1 = pkg.fast_stmf(R, int(c["rank"]), cfg)
+    _ext.release_memory()
+    p2, t2 = pkg.fast_stmf(R, int(c["rank"]), cfg)
+    assert np.array_equal(p1.U, p2.U) and np.array_equal(np.array(t1.errors), np.array(t2.errors))
+    assert np.array_equal(p1.U, c["U"])
