@@ -116,6 +116,10 @@ int stmf_objective(stmf_session* s, double* err);
  */
 int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, double epsilon,
              double* traj_t, double* traj_err, int64_t traj_cap, int64_t* counts);
+/* With traj_t = traj_err = NULL (single-device sessions) the trajectory is kept in the
+ * session, growable, and read back here: *len = its sample count; t / e (may be NULL to
+ * query the length) receive it when cap >= *len. */
+int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t cap, int64_t* len);
 
 /* ---- the reference's other fit methods ---- */
 

@@ -132,6 +132,7 @@ def lib():
         "stmf_csv_fill": [_vp, _vp, _vp, _int],
         "stmf_csv_close": [_vp],
         "stmf_release_memory": [_int],
+        "stmf_trajectory": [_vp, _vp, _vp, _i64, ctypes.POINTER(_i64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -149,7 +150,8 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
-                    "stmf_csv_close", "stmf_release_memory"]
+                    "stmf_csv_close", "stmf_release_memory",
+                    "stmf_trajectory"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -232,6 +234,7 @@ class Session:
         h = _vp()
         _check(lib().stmf_create(ctypes.byref(h), code, self.m, self.n, self.rank, _p(Xc), _p(Mc),
                                  default_device() if device is None else int(device)))
+        self.sharded = False
         self._adopt(h)
 
     def _adopt(self, h):
@@ -252,6 +255,7 @@ class Session:
         _check(lib().stmf_create_sim_group(ctypes.byref(h), STMF_F32, Xc.shape[0], Xc.shape[1], int(rank),
                                            _p(Xc), _p(Mc), int(shards),
                                            default_device() if device is None else int(device)))
+        self.sharded = True
         self._adopt(h)
         return self
 
@@ -271,6 +275,7 @@ class Session:
                                          _p(nnz), _p(Xc), _p(Mc), int(world), int(shard),
                                          None if idbuf is None else ctypes.cast(idbuf, _vp),
                                          default_device() if device is None else int(device)))
+        self.sharded = True
         self._adopt(h)
         self.local_rows = Xc.shape[0]
         return self
@@ -315,19 +320,31 @@ class Session:
         return e.value
 
     def run(self, budget_sweeps=None, budget_seconds=None, epsilon=1e-8, traj_cap=None):
-        if traj_cap is None:
-            sw = budget_sweeps if budget_sweeps is not None else 1000
-            traj_cap = 2 + (self.m + 1) * (sw + 1)
-        tt = np.empty(traj_cap, np.float64)
-        te = np.empty(traj_cap, np.float64)
+        """run_fit's sweep loop on the device.  traj_cap=None: the trajectory is kept in
+        the library (growable) and read back after the run (single-device sessions);
+        otherwise it goes to buffers of traj_cap samples."""
         counts = np.zeros(8, np.int64)
-        _check(lib().stmf_run(self._h, -1 if budget_sweeps is None else int(budget_sweeps),
-                              0.0 if budget_seconds is None else float(budget_seconds), float(epsilon),
-                              _p(tt), _p(te), traj_cap, _p(counts)))
-        L = int(counts[0])
+        bs = -1 if budget_sweeps is None else int(budget_sweeps)
+        secs = 0.0 if budget_seconds is None else float(budget_seconds)
+        if traj_cap is None and not self.sharded:
+            _check(lib().stmf_run(self._h, bs, secs, float(epsilon), None, None, 0, _p(counts)))
+            L = int(counts[0])
+            tt = np.empty(L, np.float64)
+            te = np.empty(L, np.float64)
+            n = _i64()
+            _check(lib().stmf_trajectory(self._h, _p(tt), _p(te), L, ctypes.byref(n)))
+        else:
+            if traj_cap is None:
+                sw = budget_sweeps if budget_sweeps is not None else 1000
+                traj_cap = 2 + (self.m + 1) * (sw + 1)
+            tt = np.empty(traj_cap, np.float64)
+            te = np.empty(traj_cap, np.float64)
+            _check(lib().stmf_run(self._h, bs, secs, float(epsilon), _p(tt), _p(te), traj_cap, _p(counts)))
+            L = int(counts[0])
+            tt, te = tt[:L].copy(), te[:L].copy()
         keys = ("traj_len", "attempts", "accepts", "sweeps", "row_visits", "evaluated", "replicas",
                 "product_passes")
-        return tt[:L].copy(), te[:L].copy(), dict(zip(keys, (int(c) for c in counts)))
+        return tt, te, dict(zip(keys, (int(c) for c in counts)))
 
     # diff-test hooks ------------------------------------------------------
     def product_given(self):

@@ -210,6 +210,9 @@ struct SessionBase {
       fail(STMF_ERR_INVALID, "sharded sessions run FastSTMF (ByRow / TD_A) only");
   }
   virtual void row_scores(double*) { fail(STMF_ERR_INVALID, "not available on sharded sessions"); }
+  virtual void trajectory(double*, double*, int64_t, int64_t*) {
+    fail(STMF_ERR_INVALID, "sharded sessions write the trajectory to the caller's buffers");
+  }
   virtual void matrix_candidates(int32_t*, int32_t*, int32_t*, double*) {
     fail(STMF_ERR_INVALID, "not available on sharded sessions");
   }
@@ -935,7 +938,7 @@ struct Session : SessionBase {
   // replica: the replica runs on the stream and its value becomes err at the next
   // point that needs err (the next decision, a sweep boundary, the end of the run).
   bool err_pending = false;
-  double* pend_te = nullptr;  // trajectory slot to fill with the resolved value
+  int64_t pend_idx = -1;  // trajectory sample to fill with the resolved value
   int64_t n_deferred = 0;
 
   void resolve_err() {
@@ -965,8 +968,8 @@ struct Session : SessionBase {
     }
     if (!(fr < err)) fail(STMF_ERR_NUMERIC, "decision bound violated: replica=%.17g err=%.17g", fr, err);
     err = fr;
-    if (pend_te) *pend_te = fr;
-    pend_te = nullptr;
+    if (pend_idx >= 0 && cur_run) traj_set(*cur_run, pend_idx, fr);
+    pend_idx = -1;
     err_pending = false;
   }
 
@@ -1219,9 +1222,31 @@ struct Session : SessionBase {
 
   double run_now(RunState& R) { return R.wall ? now_s() - R.t0 : (double)R.cur_sweep; }
   bool out_of_time(RunState& R) { return R.wall && now_s() - R.t0 >= R.budget_seconds; }
+  // the trajectory goes to the caller's buffers, or (null buffers) to the session's
+  // growable copy, read back with stmf_trajectory
+  std::vector<double> tj_t, tj_e;
+  RunState* cur_run = nullptr;
   void traj_append(RunState& R, double t, double e) {
+    if (!R.tt) {
+      tj_t.push_back(t);
+      tj_e.push_back(e);
+      R.len++;
+      return;
+    }
     if (R.len >= R.cap) fail(STMF_ERR_CAPACITY, "trajectory capacity %lld exceeded", (long long)R.cap);
     R.tt[R.len] = t; R.te[R.len] = e; R.len++;
+  }
+  void traj_set(RunState& R, int64_t idx, double e) {
+    if (R.tt) R.te[idx] = e;
+    else tj_e[idx] = e;
+  }
+  void trajectory(double* t, double* e, int64_t cap, int64_t* len) override {
+    *len = (int64_t)tj_t.size();
+    if (!t || !e) return;
+    if (cap < *len) fail(STMF_ERR_CAPACITY, "trajectory has %lld samples, capacity %lld", (long long)*len,
+                         (long long)cap);
+    std::memcpy(t, tj_t.data(), sizeof(double) * tj_t.size());
+    std::memcpy(e, tj_e.data(), sizeof(double) * tj_e.size());
   }
 
   // byrow_sweep(run, i, "TD_A") (strategies.py:191-224)
@@ -1307,7 +1332,7 @@ struct Session : SessionBase {
         R.accepts++;
         if (deferred) {
           traj_append(R, run_now(R), std::nan(""));
-          pend_te = &R.te[R.len - 1];
+          pend_idx = R.len - 1;
         } else {
           err = f;
           traj_append(R, run_now(R), err);
@@ -1988,7 +2013,7 @@ struct Session : SessionBase {
         if (!(fr < h.err_prev)) fail(STMF_ERR_NUMERIC, "decision bound violated: replica=%.17g err=%.17g", fr,
                                      h.err_prev);
         err = fr;
-        R.te[R.len - 1] = fr;
+        traj_set(R, R.len - 1, fr);
         start = h.i;
         if (start < m) continue;
       }
@@ -2009,6 +2034,12 @@ struct Session : SessionBase {
     R.budget_seconds = budget_seconds;
     R.t0 = now_s();
     R.tt = tt; R.te = te; R.cap = cap;
+    if (!tt) { tj_t.clear(); tj_e.clear(); }
+    cur_run = &R;
+    struct ClearRun {
+      RunState*& r;
+      ~ClearRun() { r = nullptr; }
+    } clear_run{cur_run};
     int64_t pp0 = n_product_passes, esc0 = n_escalations;
     objective();
     traj_append(R, run_now(R), err);  // FitRun.__init__ (engine.py:263)
@@ -2615,9 +2646,15 @@ int stmf_objective(stmf_session* s, double* err) {
 int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, double epsilon, double* traj_t,
              double* traj_err, int64_t traj_cap, int64_t* counts) {
   NEED(s);
-  if (!traj_t || !traj_err || !counts) return set_err(STMF_ERR_INVALID, "null output buffer");
+  if (!counts || (!traj_t) != (!traj_err)) return set_err(STMF_ERR_INVALID, "null output buffer");
   if (epsilon < 0) return set_err(STMF_ERR_INVALID, "epsilon must be >= 0");
   GUARD(s->impl->run(budget_sweeps, budget_seconds, epsilon, traj_t, traj_err, traj_cap, counts));
+}
+
+int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t cap, int64_t* len) {
+  NEED(s);
+  if (!len) return set_err(STMF_ERR_INVALID, "null argument");
+  GUARD(s->impl->trajectory(traj_t, traj_err, cap, len));
 }
 
 int stmf_product_given(stmf_session* s, void* P, int32_t* arg, void* top2) {

@@ -847,6 +847,7 @@ struct ShardGroup : SessionBase {
   void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
            int64_t* counts) override {
     if (budget_sweeps < 0 && !(budget_seconds > 0)) fail(STMF_ERR_INVALID, "set budget_sweeps or budget_seconds");
+    if (!tt || !te) fail(STMF_ERR_INVALID, "sharded sessions need trajectory buffers");
     RunState R{};
     R.wall = budget_seconds > 0;
     R.budget_seconds = budget_seconds;

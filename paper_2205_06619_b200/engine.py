@@ -194,12 +194,8 @@ def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int
             budget_seconds = None
             if wall_clock:
                 budget_seconds = max(config.budget_seconds - (time.perf_counter() - t0), 1e-9)
-            # accepts per sweep: <= 1 per row visit (ByRow), <= 1 per given entry
-            # (ByElement, baseline)
-            per = work.m if family == _ext.FAMILY_BYROW else work.given_count
-            sw = config.budget_sweeps if config.budget_sweeps is not None else 64
-            tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon,
-                                   traj_cap=2 + (per + 1) * (sw + 1))
+            # the trajectory is kept (growable) in the library and read back
+            tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)
         U, V = s.get_factors()
     t_max = config.budget_seconds if wall_clock else float(config.budget_sweeps)
     traj = Trajectory(t_init=t_init, t_max=t_max, time_unit="seconds" if wall_clock else "sweeps")
