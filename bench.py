@@ -342,6 +342,10 @@ def run_b200(args):
         }
     # e2e through the public API: host MaskedMatrix -> fast_stmf (H2D of X + mask,
     # init, K sweeps from the seeded init, D2H of U, V) timed on the host
+    # the timed session's device memory returns to the library's pool, which the e2e
+    # fit below then reuses (as a second fit in a user's process would)
+    s.close()
+    del flush
     if not args.no_e2e:
         barrier()
         t0 = time.perf_counter()
@@ -370,7 +374,6 @@ def run_b200(args):
                       f"{first_step_attempts} (that sweep's attempt count, identical decisions)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    s.close()
     if world > 1:
         dist.destroy_process_group()
 
