@@ -35,6 +35,8 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# benchmarks execute every sweep: no replay of fixpoint sweeps (stmf_replayed_sweeps)
+os.environ["STMF_FIXPOINT_REPLAY"] = "0"
 sys.path.insert(0, ROOT)
 
 METRIC = "FastSTMF fit iters/sec (sweeps/s) and observed-entry Gentries/s"

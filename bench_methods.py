@@ -16,6 +16,8 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# benchmarks execute every sweep: no replay of fixpoint sweeps (stmf_replayed_sweeps)
+os.environ["STMF_FIXPOINT_REPLAY"] = "0"
 sys.path.insert(0, ROOT)
 
 METHODS = ["FastSTMF", "STMF", "STMF_ByElement_PermC_TD", "STMF_ByMatrix_NoPerm_TD_W",

@@ -120,6 +120,12 @@ int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, doub
  * session, growable, and read back here: *len = its sample count; t / e (may be NULL to
  * query the length) receive it when cap >= *len. */
 int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t cap, int64_t* len);
+/* Fixpoint sweeps (no accepted update: every later sweep repeats it exactly, since the
+ * sweeps draw no random numbers) are replayed — trajectory samples and attempt counts —
+ * instead of recomputed when the run has a sweep budget and epsilon = 0; this reports
+ * how many sweeps of the session's runs were replayed.  STMF_FIXPOINT_REPLAY=0 in the
+ * environment executes them. */
+int stmf_replayed_sweeps(stmf_session* s, int64_t* n);
 
 /* ---- the reference's other fit methods ---- */
 

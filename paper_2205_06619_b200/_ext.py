@@ -133,6 +133,7 @@ def lib():
         "stmf_csv_close": [_vp],
         "stmf_release_memory": [_int],
         "stmf_trajectory": [_vp, _vp, _vp, _i64, ctypes.POINTER(_i64)],
+        "stmf_replayed_sweeps": [_vp, ctypes.POINTER(_i64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -151,7 +152,7 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
                     "stmf_csv_close", "stmf_release_memory",
-                    "stmf_trajectory"]
+                    "stmf_trajectory", "stmf_replayed_sweeps"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -344,7 +345,12 @@ class Session:
             tt, te = tt[:L].copy(), te[:L].copy()
         keys = ("traj_len", "attempts", "accepts", "sweeps", "row_visits", "evaluated", "replicas",
                 "product_passes")
-        return tt, te, dict(zip(keys, (int(c) for c in counts)))
+        out = dict(zip(keys, (int(c) for c in counts)))
+        if not self.sharded:
+            rep = _i64()
+            _check(lib().stmf_replayed_sweeps(self._h, ctypes.byref(rep)))
+            out["replayed_sweeps_total"] = int(rep.value)
+        return tt, te, out
 
     # diff-test hooks ------------------------------------------------------
     def product_given(self):

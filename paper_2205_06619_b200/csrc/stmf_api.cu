@@ -204,6 +204,7 @@ struct SessionBase {
   virtual void* stream() = 0;
   virtual void set_profiling(int on) = 0;
   virtual void counters(int64_t* out) = 0;
+  virtual int64_t replayed_sweeps() { return 0; }
   // the reference's other fit methods
   virtual void set_strategy(int family, int selection) {
     if (family != STMF_FAMILY_BYROW || selection != STMF_SEL_TD_A)
@@ -1609,6 +1610,9 @@ struct Session : SessionBase {
     ssync();
   }
 
+  bool fixpoint_replay = getenv("STMF_FIXPOINT_REPLAY") ? atoi(getenv("STMF_FIXPOINT_REPLAY")) != 0 : true;
+  int64_t n_replayed_sweeps = 0;
+  int64_t replayed_sweeps() override { return n_replayed_sweeps; }
   std::vector<int64_t> row_depth;  // candidates consumed at each row's last visit
   bool rdepth_on_dev = false;      // the device copy (graph sweeps) is the current one
   void pull_row_depth() {
@@ -2051,6 +2055,8 @@ struct Session : SessionBase {
         if (out_of_time(R)) break;
         R.cur_sweep = sweeps + 1;
         double err_before = err;
+        int64_t accepts_before = R.accepts, attempts_before = R.attempts, visits_before = R.visits,
+                evaluated_before = R.evaluated;
         if (!R.wall && graph_eligible()) {
           if (!rdepth_on_dev) {
             h_rdepth.assign(row_depth.begin(), row_depth.end());
@@ -2071,6 +2077,26 @@ struct Session : SessionBase {
         resolve_err();
         traj_append(R, run_now(R), err);  // mark_sweep_boundary (engine.py:309-310)
         if (err_before - err < eps) break;
+        // Fixpoint: a sweep without an accepted update leaves
+        // U, V and err unchanged, and ByRow / ByElement / the baseline draw no random
+        // numbers during sweeps, so every later sweep repeats it exactly.  With a sweep
+        // budget and epsilon = 0 the remaining sweeps are replayed (their trajectory
+        // samples and attempt counts) instead of recomputed; STMF_FIXPOINT_REPLAY=0
+        // executes them (benchmarks do, so fixpoint sweeps are never counted as run).
+        if (!R.wall && budget_sweeps >= 0 && err == err_before && R.accepts == accepts_before &&
+            fixpoint_replay) {
+          int64_t sw_att = R.attempts - attempts_before, sw_vis = R.visits - visits_before,
+                  sw_ev = R.evaluated - evaluated_before;
+          while (sweeps < budget_sweeps) {
+            R.cur_sweep = ++sweeps;
+            R.attempts += sw_att;
+            R.visits += sw_vis;
+            R.evaluated += sw_ev;
+            traj_append(R, run_now(R), err);
+            n_replayed_sweeps++;
+          }
+          break;
+        }
       }
     }
     resolve_err();
@@ -2649,6 +2675,12 @@ int stmf_run(stmf_session* s, int64_t budget_sweeps, double budget_seconds, doub
   if (!counts || (!traj_t) != (!traj_err)) return set_err(STMF_ERR_INVALID, "null output buffer");
   if (epsilon < 0) return set_err(STMF_ERR_INVALID, "epsilon must be >= 0");
   GUARD(s->impl->run(budget_sweeps, budget_seconds, epsilon, traj_t, traj_err, traj_cap, counts));
+}
+
+int stmf_replayed_sweeps(stmf_session* s, int64_t* n) {
+  NEED(s);
+  if (!n) return set_err(STMF_ERR_INVALID, "null argument");
+  GUARD(*n = s->impl->replayed_sweeps());
 }
 
 int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t cap, int64_t* len) {

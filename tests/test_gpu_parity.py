@@ -87,12 +87,22 @@ def test_config1_full_100_sweeps_matches_reference_run(monkeypatch, graph):
     from paper_2205_06619_b200 import gen
     R = gen.config1()
     cfg = pkg.RunConfig(rank=3, budget_sweeps=100, epsilon=0.0, seed=42)
-    pair, traj = pkg.fast_stmf(R, 3, cfg)
-    assert traj.final_error == 313.80609464110563
-    assert traj.counts["attempts"] == 3078993
-    assert traj.counts["sweeps"] == 100
-    # the fixpoint sweeps (12..100) are executed, not short-circuited
-    assert traj.counts["row_visits"] == 100 * 100
+    runs = {}
+    for replay in ("0", "1"):
+        monkeypatch.setenv("STMF_FIXPOINT_REPLAY", replay)
+        pair, traj = pkg.fast_stmf(R, 3, cfg)
+        assert traj.final_error == 313.80609464110563
+        assert traj.counts["attempts"] == 3078993
+        assert traj.counts["sweeps"] == 100
+        assert traj.counts["row_visits"] == 100 * 100
+        runs[replay] = (pair, traj)
+    # executed (replay 0: sweeps 12..100 run for real) and replayed fixpoint sweeps give
+    # the same factors, trajectory and counts
+    (p0, t0), (p1, t1) = runs["0"], runs["1"]
+    assert t0.counts["replayed_sweeps_total"] == 0 and t1.counts["replayed_sweeps_total"] == 100 - 12
+    assert np.array_equal(p0.U, p1.U) and np.array_equal(p0.V, p1.V)
+    assert np.array_equal(np.array(t0.errors), np.array(t1.errors))
+    assert np.array_equal(np.array(t0.times), np.array(t1.times))
 
 
 def _f32_case(seed, m, n, r, frac):
