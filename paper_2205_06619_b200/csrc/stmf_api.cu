@@ -14,6 +14,7 @@
 //      reference order with f < err wins (FitRun._attempt, engine.py:283);
 //   4. commit: column k of U, row k of V.
 #include <cub/device/device_radix_sort.cuh>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -2283,6 +2284,28 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   CK(cudaFuncSetAttribute(k_maxplus_err<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   CK(cudaFuncSetAttribute(k_maxplus_err<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   auto kern = r <= 4 ? k_maxplus_err<4> : r <= 8 ? k_maxplus_err<8> : k_maxplus_err<16>;
+  // TMA-fed X tiles (STMF_C5_TMA=0: per-thread cp.async copies)
+  bool tma = getenv("STMF_C5_TMA") ? atoi(getenv("STMF_C5_TMA")) != 0 : true;
+  CUtensorMap xmap{};
+  if (tma) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+    cuuint64_t strides[1] = {(cuuint64_t)n * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)kMpTC, (cuuint32_t)kMpTR};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, X.p, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    CK(cudaFuncSetAttribute(k_maxplus_err<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+    CK(cudaFuncSetAttribute(k_maxplus_err<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+    CK(cudaFuncSetAttribute(k_maxplus_err<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
+  }
+  auto kernt = r <= 4 ? k_maxplus_err<4, true> : r <= 8 ? k_maxplus_err<8, true> : k_maxplus_err<16, true>;
   double total = 0, best = 1e30;
   u64 h[2] = {0, 0};
   for (int rep = 0; rep < std::max(reps, 1); rep++) {
@@ -2290,7 +2313,10 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
-    kern<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit);
+    if (tma)
+      kernt<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap);
+    else
+      kern<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap);
     LAUNCH_CK();
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));

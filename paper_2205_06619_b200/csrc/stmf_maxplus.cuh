@@ -44,15 +44,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // m % 64 == 0, n % 128 == 0 (k-slices beyond r are -inf); KC = k-chunk (even)
-template <int KC>
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// TMA = true: the block's 64 x 128 X tile arrives by one bulk tensor copy
+// (cp.async.bulk.tensor, tensor map xmap) completing on an mbarrier, instead of 2048
+// 16-byte cp.async copies issued by all threads
+template <int KC, bool TMA = false>
 __global__ void __launch_bounds__(256, KC <= 4 ? 4 : 3)
 k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const uint32_t* __restrict__ mask,
               const float* __restrict__ Ut, const float* __restrict__ V, u64* __restrict__ acc,
-              int* __restrict__ flags, int F, double exact_limit) {
+              int* __restrict__ flags, int F, double exact_limit, const __grid_constant__ CUtensorMap xmap = {}) {
   __shared__ __align__(16) float Us[2][KC][kMpTR];
   __shared__ __align__(16) float Vs[2][KC][kMpTC];
   // dynamic shared memory (kMaxplusDynSmem): the block's 64 x 128 X tile (32 KB) and its mask words
-  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
   float (*Xs)[kMpTC] = reinterpret_cast<float (*)[kMpTC]>(dyn_smem);
   uint32_t (*Ms)[kMpTC / 32] = reinterpret_cast<uint32_t (*)[kMpTC / 32]>(dyn_smem + sizeof(float) * kMpTR * kMpTC);
   __shared__ double red[8];
@@ -60,11 +65,26 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   int64_t row0 = (int64_t)blockIdx.y * kMpTR, col0 = (int64_t)blockIdx.x * kMpTC;
   // the epilogue's HBM traffic is issued first (async copies into shared memory),
   // so it streams while the k-loop computes
+  __shared__ __align__(8) uint64_t xbar;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&xbar)));
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&xbar)),
+                   "r"((unsigned)(sizeof(float) * kMpTR * kMpTC)));
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+          "[%4];" ::"r"(smem_u32(&Xs[0][0])),
+          "l"(&xmap), "r"((int)col0), "r"((int)row0), "r"(smem_u32(&xbar))
+          : "memory");
+    }
+  } else {
 #pragma unroll
-  for (int h = 0; h < 8; h++) {
-    int e = threadIdx.x + 256 * h;  // 2048 16-byte chunks
-    int rr = e >> 5, c4 = (e & 31) * 4;
-    cp_async16(&Xs[rr][c4], X + (row0 + rr) * n + col0 + c4);
+    for (int h = 0; h < 8; h++) {
+      int e = threadIdx.x + 256 * h;  // 2048 16-byte chunks
+      int rr = e >> 5, c4 = (e & 31) * 4;
+      cp_async16(&Xs[rr][c4], X + (row0 + rr) * n + col0 + c4);
+    }
   }
   if (threadIdx.x < kMpTR) {
     const uint32_t* mw = mask + ((row0 + threadIdx.x) * n + col0) / 32;
@@ -128,6 +148,12 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   }
   // epilogue: given residuals, exact accumulation
   cp_async_wait_all();
+  if constexpr (TMA) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(&xbar))
+        : "memory");
+  }
   __syncthreads();
   double part = 0.0;
 #pragma unroll
