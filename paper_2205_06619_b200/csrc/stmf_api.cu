@@ -2286,7 +2286,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   auto kern = r <= 4 ? k_maxplus_err<4> : r <= 8 ? k_maxplus_err<8> : k_maxplus_err<16>;
   // TMA-fed X tiles (STMF_C5_TMA=0: per-thread cp.async copies)
   bool tma = getenv("STMF_C5_TMA") ? atoi(getenv("STMF_C5_TMA")) != 0 : true;
-  CUtensorMap xmap{};
+  CUtensorMap xmap{}, umap{}, vmap{};
   if (tma) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -2301,6 +2301,19 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    // factor slices (used when r equals the kernel's k-chunk): Ut is r x m, V is r x n
+    int kc = r <= 4 ? 4 : r <= 8 ? 8 : 16;
+    if (r == kc) {
+      cuuint64_t ud[2] = {(cuuint64_t)m, (cuuint64_t)r}, vd[2] = {(cuuint64_t)n, (cuuint64_t)r};
+      cuuint64_t us[1] = {(cuuint64_t)m * sizeof(float)}, vs[1] = {(cuuint64_t)n * sizeof(float)};
+      cuuint32_t ub[2] = {(cuuint32_t)kMpTR, (cuuint32_t)kc}, vb[2] = {(cuuint32_t)kMpTC, (cuuint32_t)kc};
+      cr = encode(&umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Ut.p, ud, us, ub, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr == CUDA_SUCCESS)
+        cr = encode(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, V.p, vd, vs, vb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    }
     CK(cudaFuncSetAttribute(k_maxplus_err<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
     CK(cudaFuncSetAttribute(k_maxplus_err<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
     CK(cudaFuncSetAttribute(k_maxplus_err<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
@@ -2314,9 +2327,11 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
     if (tma)
-      kernt<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap);
+      kernt<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap,
+                                                umap, vmap);
     else
-      kern<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap);
+      kern<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap,
+                                               umap, vmap);
     LAUNCH_CK();
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));

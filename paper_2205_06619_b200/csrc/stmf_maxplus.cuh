@@ -53,9 +53,10 @@ template <int KC, bool TMA = false>
 __global__ void __launch_bounds__(256, KC <= 4 ? 4 : 3)
 k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const uint32_t* __restrict__ mask,
               const float* __restrict__ Ut, const float* __restrict__ V, u64* __restrict__ acc,
-              int* __restrict__ flags, int F, double exact_limit, const __grid_constant__ CUtensorMap xmap = {}) {
-  __shared__ __align__(16) float Us[2][KC][kMpTR];
-  __shared__ __align__(16) float Vs[2][KC][kMpTC];
+              int* __restrict__ flags, int F, double exact_limit, const __grid_constant__ CUtensorMap xmap = {},
+              const __grid_constant__ CUtensorMap umap = {}, const __grid_constant__ CUtensorMap vmap = {}) {
+  __shared__ __align__(128) float Us[2][KC][kMpTR];
+  __shared__ __align__(128) float Vs[2][KC][kMpTC];
   // dynamic shared memory (kMaxplusDynSmem): the block's 64 x 128 X tile (32 KB) and its mask words
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   float (*Xs)[kMpTC] = reinterpret_cast<float (*)[kMpTC]>(dyn_smem);
@@ -65,11 +66,29 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   int64_t row0 = (int64_t)blockIdx.y * kMpTR, col0 = (int64_t)blockIdx.x * kMpTC;
   // the epilogue's HBM traffic is issued first (async copies into shared memory),
   // so it streams while the k-loop computes
-  __shared__ __align__(8) uint64_t xbar;
+  __shared__ __align__(8) uint64_t xbar, fbar;
+  // with r == KC the factor slices are one chunk: they arrive by TMA too (the k >= r
+  // rows that staging fills with -inf do not exist then)
+  const bool tma_f = TMA && r == KC;
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&xbar)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar)));
       asm volatile("fence.proxy.async.shared::cta;");
+      if (tma_f) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&fbar)),
+                     "r"((unsigned)(sizeof(float) * KC * (kMpTR + kMpTC))));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(smem_u32(&Us[0][0][0])),
+            "l"(&umap), "r"((int)row0), "r"(0), "r"(smem_u32(&fbar))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(smem_u32(&Vs[0][0][0])),
+            "l"(&vmap), "r"((int)col0), "r"(0), "r"(smem_u32(&fbar))
+            : "memory");
+      }
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&xbar)),
                    "r"((unsigned)(sizeof(float) * kMpTR * kMpTC)));
       asm volatile(
@@ -114,8 +133,13 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   };
 
   int nchunks = (r + KC - 1) / KC;
-  stage(0, 0);
+  if (!tma_f) stage(0, 0);
   __syncthreads();
+  if (tma_f)
+    asm volatile(
+        "{\n .reg .pred p;\n FWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra FWAIT_%=;\n}" ::"r"(smem_u32(&fbar))
+        : "memory");
   for (int ch = 0; ch < nchunks; ch++) {
     int buf = ch & 1;
     if (ch + 1 < nchunks) stage(buf ^ 1, (ch + 1) * KC);
