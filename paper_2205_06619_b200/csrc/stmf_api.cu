@@ -2290,8 +2290,17 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   if (tma) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      fn = nullptr;
+    }
+    tma = fn != nullptr;  // no tensor-map encoder in this driver: per-thread copies
+  }
+  if (tma) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
     CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
     cuuint64_t strides[1] = {(cuuint64_t)n * sizeof(float)};
