@@ -2312,7 +2312,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     if (cr != CUDA_SUCCESS) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
     // factor slices (used when r equals the kernel's k-chunk): Ut is r x m, V is r x n
     int kc = r <= 4 ? 4 : r <= 8 ? 8 : 16;
-    if (r == kc) {
+    if (r % kc == 0) {
       cuuint64_t ud[2] = {(cuuint64_t)m, (cuuint64_t)r}, vd[2] = {(cuuint64_t)n, (cuuint64_t)r};
       cuuint64_t us[1] = {(cuuint64_t)m * sizeof(float)}, vs[1] = {(cuuint64_t)n * sizeof(float)};
       cuuint32_t ub[2] = {(cuuint32_t)kMpTR, (cuuint32_t)kc}, vb[2] = {(cuuint32_t)kMpTC, (cuuint32_t)kc};

@@ -66,29 +66,39 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   int64_t row0 = (int64_t)blockIdx.y * kMpTR, col0 = (int64_t)blockIdx.x * kMpTC;
   // the epilogue's HBM traffic is issued first (async copies into shared memory),
   // so it streams while the k-loop computes
-  __shared__ __align__(8) uint64_t xbar, fbar;
-  // with r == KC the factor slices are one chunk: they arrive by TMA too (the k >= r
-  // rows that staging fills with -inf do not exist then)
-  const bool tma_f = TMA && r == KC;
+  __shared__ __align__(8) uint64_t xbar, fbar[2];
+  // when r is a multiple of KC every k-chunk of the factor slices arrives by TMA too
+  // (double-buffered, one mbarrier per buffer; the k >= r rows that staging fills
+  // with -inf do not exist then)
+  const bool tma_f = TMA && r % KC == 0;
+  auto issue_f = [&](int buf, int k0) {  // thread 0: chunk k0.. into buffer buf
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&fbar[buf])),
+                 "r"((unsigned)(sizeof(float) * KC * (kMpTR + kMpTC))));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(&Us[buf][0][0])),
+        "l"(&umap), "r"((int)row0), "r"(k0), "r"(smem_u32(&fbar[buf]))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(&Vs[buf][0][0])),
+        "l"(&vmap), "r"((int)col0), "r"(k0), "r"(smem_u32(&fbar[buf]))
+        : "memory");
+  };
+  auto wait_f = [&](int buf, int parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n FWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra FWAIT_%=;\n}" ::"r"(smem_u32(&fbar[buf])),
+        "r"(parity)
+        : "memory");
+  };
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&xbar)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[0])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[1])));
       asm volatile("fence.proxy.async.shared::cta;");
-      if (tma_f) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&fbar)),
-                     "r"((unsigned)(sizeof(float) * KC * (kMpTR + kMpTC))));
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];" ::"r"(smem_u32(&Us[0][0][0])),
-            "l"(&umap), "r"((int)row0), "r"(0), "r"(smem_u32(&fbar))
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];" ::"r"(smem_u32(&Vs[0][0][0])),
-            "l"(&vmap), "r"((int)col0), "r"(0), "r"(smem_u32(&fbar))
-            : "memory");
-      }
+      if (tma_f) issue_f(0, 0);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&xbar)),
                    "r"((unsigned)(sizeof(float) * kMpTR * kMpTC)));
       asm volatile(
@@ -135,14 +145,15 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   int nchunks = (r + KC - 1) / KC;
   if (!tma_f) stage(0, 0);
   __syncthreads();
-  if (tma_f)
-    asm volatile(
-        "{\n .reg .pred p;\n FWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-        " @!p bra FWAIT_%=;\n}" ::"r"(smem_u32(&fbar))
-        : "memory");
   for (int ch = 0; ch < nchunks; ch++) {
     int buf = ch & 1;
-    if (ch + 1 < nchunks) stage(buf ^ 1, (ch + 1) * KC);
+    if (tma_f) {
+      // buffer buf^1 was last read in chunk ch-1, which ended with __syncthreads
+      if (threadIdx.x == 0 && ch + 1 < nchunks) issue_f(buf ^ 1, (ch + 1) * KC);
+      wait_f(buf, (ch >> 1) & 1);
+    } else if (ch + 1 < nchunks) {
+      stage(buf ^ 1, (ch + 1) * KC);
+    }
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 2) {
       float4 ua = *reinterpret_cast<const float4*>(&Us[buf][kk][ty * 4]);
