@@ -2283,7 +2283,10 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   CK(cudaFuncSetAttribute(k_maxplus_err<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   CK(cudaFuncSetAttribute(k_maxplus_err<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   CK(cudaFuncSetAttribute(k_maxplus_err<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
-  auto kern = r <= 4 ? k_maxplus_err<4> : r <= 8 ? k_maxplus_err<8> : k_maxplus_err<16>;
+  // k-chunk of the factor slices: the smallest of 4 / 8 / 16 that covers r (STMF_C5_KC forces one)
+  int kc_sel = r <= 4 ? 4 : r <= 8 ? 8 : 16;
+  if (const char* e = getenv("STMF_C5_KC")) kc_sel = atoi(e) <= 4 ? 4 : atoi(e) <= 8 ? 8 : 16;
+  auto kern = kc_sel == 4 ? k_maxplus_err<4> : kc_sel == 8 ? k_maxplus_err<8> : k_maxplus_err<16>;
   // TMA-fed X tiles (STMF_C5_TMA=0: per-thread cp.async copies)
   bool tma = getenv("STMF_C5_TMA") ? atoi(getenv("STMF_C5_TMA")) != 0 : true;
   CUtensorMap xmap{}, umap{}, vmap{};
@@ -2311,7 +2314,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) fail(STMF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
     // factor slices (used when r equals the kernel's k-chunk): Ut is r x m, V is r x n
-    int kc = r <= 4 ? 4 : r <= 8 ? 8 : 16;
+    int kc = kc_sel;
     if (r % kc == 0) {
       cuuint64_t ud[2] = {(cuuint64_t)m, (cuuint64_t)r}, vd[2] = {(cuuint64_t)n, (cuuint64_t)r};
       cuuint64_t us[1] = {(cuuint64_t)m * sizeof(float)}, vs[1] = {(cuuint64_t)n * sizeof(float)};
@@ -2327,7 +2330,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaFuncSetAttribute(k_maxplus_err<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
     CK(cudaFuncSetAttribute(k_maxplus_err<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   }
-  auto kernt = r <= 4 ? k_maxplus_err<4, true> : r <= 8 ? k_maxplus_err<8, true> : k_maxplus_err<16, true>;
+  auto kernt = kc_sel == 4 ? k_maxplus_err<4, true> : kc_sel == 8 ? k_maxplus_err<8, true> : k_maxplus_err<16, true>;
   double total = 0, best = 1e30;
   u64 h[2] = {0, 0};
   for (int rep = 0; rep < std::max(reps, 1); rep++) {
