@@ -12,7 +12,7 @@ from .engine import FitSession, f_ulf, f_urf, random_acol_init, run_fit, stmf_ba
 from .strategies import BASELINE, FASTSTMF, StrategySpec, fast_stmf, fit, parse_method
 from .tropical import approx_error, argmax_grid, masked_minplus, trop_matmul
 from ._ext import build, StmfError
-from . import io, metrics
+from . import datagen, io, metrics
 
 __version__ = "0.1.0"
 
@@ -20,5 +20,5 @@ __all__ = [
     "MaskedMatrix", "Permutation", "trop_matmul", "masked_minplus", "approx_error", "argmax_grid",
     "FactorPair", "Trajectory", "UpdateOutcome", "Orientation", "RunConfig", "random_acol_init",
     "f_ulf", "f_urf", "run_fit", "stmf_baseline", "StrategySpec", "BASELINE", "FASTSTMF",
-    "parse_method", "fit", "fast_stmf", "FitSession", "build", "StmfError", "io", "metrics", "__version__",
+    "parse_method", "fit", "fast_stmf", "FitSession", "build", "StmfError", "datagen", "io", "metrics", "__version__",
 ]

@@ -88,3 +88,23 @@ def test_binary_format(tmp_path):
         assert L.dtype == R.dtype and np.array_equal(L.mask, R.mask)
         assert np.array_equal(L.values[R.mask], R.values[R.mask])
         assert p.stat().st_size == 32 + (R.m * R.n + 7) // 8 + R.given_count * R.values.itemsize
+
+
+def test_datagen_matches_reference():
+    """SynthSpec / gen_mixture / apply_mask / gen_tall_wide_pair draw the reference's
+    random numbers and reproduce its datasets (tests/golden/datagen.npz)."""
+    from conftest import GOLDEN
+    from paper_2205_06619_b200 import datagen
+    g = np.load(f"{GOLDEN}/datagen.npz")
+    for t, (r, c, lam, k, seed, frac) in enumerate(g["specs"]):
+        spec = datagen.SynthSpec(int(r), int(c), float(lam), true_rank=int(k), seed=int(seed),
+                                 mask_fraction=float(frac))
+        R, A, B = datagen.gen_mixture(spec)
+        assert np.array_equal(A, g[f"s{t}_A"]) and np.array_equal(B, g[f"s{t}_B"])
+        assert np.array_equal(R, g[f"s{t}_R"])
+        train, test = datagen.apply_mask(R, float(frac), seed=int(seed) + 100)
+        assert np.array_equal(train.mask, g[f"s{t}_given"]) and np.array_equal(test, g[f"s{t}_test"])
+        tall, wide = datagen.gen_tall_wide_pair(spec)
+        assert np.array_equal(tall, g[f"s{t}_tall"]) and np.array_equal(wide, g[f"s{t}_wide"])
+    with pytest.raises(ValueError):
+        datagen.SynthSpec(2, 5, 0.5, true_rank=3)
