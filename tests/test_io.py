@@ -108,3 +108,64 @@ def test_datagen_matches_reference():
         assert np.array_equal(tall, g[f"s{t}_tall"]) and np.array_equal(wide, g[f"s{t}_wide"])
     with pytest.raises(ValueError):
         datagen.SynthSpec(2, 5, 0.5, true_rank=3)
+
+
+def _traj(t, e, t_max):
+    tr = pkg.Trajectory(t_init=0.0, t_max=t_max, time_unit="sweeps")
+    for a, b in zip(t, e):
+        tr.append(float(a), float(b))
+    return tr
+
+
+def test_host_statistics_match_reference():
+    """metrics.py's trajectory statistics (tests/golden/hoststats.npz, from the reference)."""
+    from conftest import GOLDEN
+    from paper_2205_06619_b200 import metrics as M
+    g = np.load(f"{GOLDEN}/hoststats.npz")
+    base = _traj(g["base_t"], g["base_e"], 10.0)
+    other = _traj(g["other_t"], g["other_e"], 10.0)
+    assert np.array_equal(M.make_grid(10.0, 0.7), g["grid"])
+    assert np.array_equal(M.make_grid(3.0, 1.0, 0.5), g["grid2"])
+    assert np.array_equal(M.step_interpolate(base.times, base.errors, g["grid"]), g["interp"])
+    assert np.array_equal(M.normalized_error(other, base, g["grid"]), g["ne"])
+    assert np.array_equal(np.array(M.bootstrap_ci(g["samples"], n_resamples=300, level=0.9, seed=3)), g["ci"])
+    assert np.array_equal(M.rank_methods(g["scores"]), g["ranks"])
+    assert np.array_equal(M.rank_methods(g["scores"], lower_is_better=False), g["ranks_hi"])
+    assert np.array_equal(M.average_ranks(g["ranks"]), g["avg"])
+    assert np.array_equal(np.array([M.nemenyi_cd(4, 6), M.nemenyi_cd(3, 10, 0.1)]), g["cd"])
+    ttr = [M.time_to_reach(base, float(base.errors[5]), g["grid"]), M.time_to_reach(base, -1.0, g["grid"])]
+    assert np.array_equal(np.array(ttr), g["ttr"]) and ttr[1] == M.NEVER
+    assert M.omega(g["samples"][:20], g["samples"][20:]) == float(g["omega"])
+
+
+def test_sidecar_files_match_reference(tmp_path):
+    """io.py's JSONL / JSON / CSV bundles: the same bytes as the reference's, and they
+    read back (tests/golden/hoststats_files, from the reference)."""
+    import filecmp
+    from conftest import GOLDEN
+    from paper_2205_06619_b200 import datagen
+    ref = f"{GOLDEN}/hoststats_files"
+    g = np.load(f"{GOLDEN}/hoststats.npz")
+    base = _traj(g["base_t"], g["base_e"], 10.0)
+    sio.save_trajectory(tmp_path / "traj.jsonl", base)
+    assert filecmp.cmp(tmp_path / "traj.jsonl", f"{ref}/traj.jsonl", shallow=False)
+    back = sio.load_trajectory(tmp_path / "traj.jsonl")
+    assert back.times == base.times and back.errors == base.errors
+    U = sio.load_matrix_csv(f"{ref}/p_U.csv").values
+    V = sio.load_matrix_csv(f"{ref}/p_V.csv").values
+    ori = pkg.Orientation(True, pkg.Permutation(np.array([1, 0])), None)
+    sio.save_factors(tmp_path, pkg.FactorPair(U, V, 2, ori), config={"seed": 3, "method": "FastSTMF"}, prefix="p_")
+    for f in ("p_U.csv", "p_V.csv", "p_factors.json"):
+        assert filecmp.cmp(tmp_path / f, f"{ref}/{f}", shallow=False), f
+    U2, V2, side = sio.load_factors(tmp_path, prefix="p_")
+    assert np.array_equal(U2, U) and side["rank"] == 2
+    ds = f"{ref}/ds"
+    train, test_mask, test_values, meta = sio.load_dataset(ds)
+    X = np.where(test_mask, test_values, train.values)
+    A = sio.load_matrix_csv(f"{ds}/true_A.csv").values
+    B = sio.load_matrix_csv(f"{ds}/true_B.csv").values
+    tr2, te2 = datagen.apply_mask(X, 0.3, seed=2)
+    assert np.array_equal(tr2.mask, train.mask) and np.array_equal(te2, test_mask)
+    sio.save_dataset(tmp_path / "ds", tr2, te2, X, {"name": "toy", "lam": 0.5}, A=A, B=B)
+    for f in ("dataset.json", "train.csv", "true_A.csv", "true_B.csv"):
+        assert filecmp.cmp(tmp_path / "ds" / f, f"{ds}/{f}", shallow=False), f
