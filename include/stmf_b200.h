@@ -214,6 +214,9 @@ int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t 
  * pred/truth: m x n binary64, mask: m x n bytes (nonzero = evaluated). */
 int stmf_masked_rmse(int64_t m, int64_t n, const double* pred, const double* truth, const uint8_t* mask,
                      int device, double* out);
+/* b_norm (tropical.py:197-211): np.sum(np.sort(|values|)) of n binary64 values on
+ * the device, bit-identical to numpy (radix sort + numpy's pairwise tree); 0 for n = 0. */
+int stmf_b_norm(int64_t n, const double* values, int device, double* out);
 /* distance_correlation(x, y) (metrics.py:98-117) of two length-len samples (len >= 2):
  * doubly-centred distance matrices and numpy's means, bit-identical to numpy. */
 int stmf_distance_correlation(int64_t len, const double* x, const double* y, int device, double* out);

@@ -134,6 +134,7 @@ def lib():
         "stmf_release_memory": [_int],
         "stmf_trajectory": [_vp, _vp, _vp, _i64, ctypes.POINTER(_i64)],
         "stmf_replayed_sweeps": [_vp, ctypes.POINTER(_i64)],
+        "stmf_b_norm": [_i64, _vp, _int, ctypes.POINTER(_dbl)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -152,7 +153,8 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
                     "stmf_csv_close", "stmf_release_memory",
-                    "stmf_trajectory", "stmf_replayed_sweeps"]
+                    "stmf_trajectory", "stmf_replayed_sweeps",
+                    "stmf_b_norm"]
 
 # include/stmf_b200.h: families and ByRow selection rules
 FAMILY_BYROW, FAMILY_BYELEMENT, FAMILY_BASELINE, FAMILY_BYMATRIX = 0, 1, 2, 3
@@ -463,3 +465,10 @@ def csv_read(path: str, has_header: bool = False, threads: int = 0):
 def release_memory(device: int | None = None):
     """Return the device memory pool's unused blocks (kept for reuse by later sessions)."""
     _check(lib().stmf_release_memory(default_device() if device is None else device))
+
+
+def b_norm(values, device: int | None = None) -> float:
+    v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+    out = _dbl()
+    _check(lib().stmf_b_norm(v.size, _p(v), default_device() if device is None else device, ctypes.byref(out)))
+    return out.value

@@ -2544,6 +2544,31 @@ static void centered_distances(int64_t n, const double* dx, DevBuf<double>& A, c
   CK(cudaStreamSynchronize(st));
 }
 
+// b_norm(W, mask) (tropical.py:197-211): numpy's pairwise sum of the ascending
+// |values|; |v| >= 0, so the bit patterns sort like the values (CUB radix sort)
+__global__ void k_abs_bits(int64_t n, const double* __restrict__ v, u64* __restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (u64)__double_as_longlong(fabs(v[t]));
+}
+
+static double b_norm_impl(int64_t n, const double* vals, int device) {
+  ScopedStream S(device);
+  cudaStream_t st = S.st;
+  DevBuf<double> dv;
+  DevBuf<u64> a, b;
+  dv.alloc(n); a.alloc(n); b.alloc(n);
+  CK(cudaMemcpyAsync(dv.p, vals, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  k_abs_bits<<<nblk(n, 256), 256, 0, st>>>(n, dv.p, a.p);
+  LAUNCH_CK();
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, a.p, b.p, n, 0, 63, st));
+  DevBuf<uint8_t> tmp;
+  tmp.alloc(bytes);
+  CK(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, a.p, b.p, n, 0, 63, st));
+  g_cub_calls++;
+  return device_pairwise_sum(reinterpret_cast<const double*>(b.p), n, st);
+}
+
 // distance_correlation(x, y) (metrics.py:98-117)
 static double distance_correlation_impl(int64_t n, const double* x, const double* y, int device) {
   ScopedStream S(device);
@@ -2793,6 +2818,12 @@ int stmf_masked_rmse(int64_t m, int64_t n, const double* pred, const double* tru
   if (m < 0 || n < 0) return set_err(STMF_ERR_INVALID, "bad shape");
   if (m == 0 || n == 0) { *out = 0.0; return STMF_OK; }
   GUARD(*out = masked_rmse_impl(m, n, pred, truth, mask, device));
+}
+
+int stmf_b_norm(int64_t n, const double* values, int device, double* out) {
+  if (!out || (n > 0 && !values)) return set_err(STMF_ERR_INVALID, "null argument");
+  if (n <= 0) { *out = 0.0; return STMF_OK; }
+  GUARD(*out = b_norm_impl(n, values, device));
 }
 
 int stmf_distance_correlation(int64_t len, const double* x, const double* y, int device, double* out) {

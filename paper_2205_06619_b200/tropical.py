@@ -11,7 +11,7 @@ from . import _ext
 from .types import MaskedMatrix, Permutation
 
 __all__ = ["MaskedMatrix", "Permutation", "trop_matmul", "argmax_grid", "approx_error",
-           "masked_minplus", "sort_perm_by_min"]
+           "masked_minplus", "sort_perm_by_min", "b_norm", "td", "argmax_k", "td_row", "td_col", "td_grid"]
 
 
 def trop_matmul(A, B) -> np.ndarray:
@@ -58,3 +58,49 @@ def sort_perm_by_min(M: MaskedMatrix, axis: str) -> Permutation:
     else:
         raise ValueError(f"axis must be 'rows' or 'cols', got {axis!r}")
     return Permutation(np.argsort(mins, kind="stable"))
+
+
+def b_norm(W, mask=None) -> float:
+    """Sum of |values| over the given entries, numpy's sorted pairwise sum, on the
+    device (tropical.py:197-211); 0 for an empty mask."""
+    if isinstance(W, MaskedMatrix):
+        values, mask = W.values, W.mask
+    else:
+        values = np.asarray(W, dtype=np.float64)
+    vals = np.asarray(values if mask is None else values[np.asarray(mask, dtype=bool)], dtype=np.float64)
+    return 0.0 if vals.size == 0 else _ext.b_norm(vals)
+
+
+def td_grid(R: MaskedMatrix, U, V, product=None) -> np.ndarray:
+    """|R - U (x) V| at the given entries, 0 elsewhere (tropical.py:237-245); the product
+    on the device unless given."""
+    P = trop_matmul(U, V) if product is None else np.asarray(product)
+    return np.where(R.mask, np.abs(np.where(R.mask, R.values, 0.0) - P), 0.0)
+
+
+# Single-entry / single-line helpers of the reference (tropical.py:225-257): O(r) or
+# O(n r) host arithmetic on a handful of values (used by the reference's non-FastSTMF
+# strategies when driven by hand; the device engine computes the same quantities inside
+# its kernels).
+def td(R: MaskedMatrix, U, V, i: int, j: int) -> float:
+    """|R[i, j] - max_k(U[i, k] + V[k, j])| of a given entry (tropical.py:225-229)."""
+    if not R.mask[i, j]:
+        raise ValueError(f"entry ({i}, {j}) is missing")
+    return float(abs(R.values[i, j] - np.max(np.asarray(U)[i, :] + np.asarray(V)[:, j])))
+
+
+def argmax_k(U, V, i: int, j: int) -> int:
+    """Lowest k attaining max_k U[i, k] + V[k, j] (tropical.py:232-234)."""
+    return int(np.argmax(np.asarray(U)[i, :] + np.asarray(V)[:, j]))
+
+
+def td_row(R: MaskedMatrix, U, V, i: int) -> float:
+    """Sum of the entry errors over the given entries of row i (tropical.py:248-251)."""
+    p = np.max(np.asarray(U)[i, :][None, :] + np.asarray(V).T, axis=1)
+    return float(np.sum(np.abs(R.values[i] - p)[R.mask[i]]))
+
+
+def td_col(R: MaskedMatrix, U, V, j: int) -> float:
+    """Sum of the entry errors over the given entries of column j (tropical.py:254-257)."""
+    p = np.max(np.asarray(U) + np.asarray(V)[:, j][None, :], axis=1)
+    return float(np.sum(np.abs(R.values[:, j] - p)[R.mask[:, j]]))

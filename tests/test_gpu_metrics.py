@@ -73,3 +73,29 @@ def test_masked_dc_subsamples_like_the_reference():
     idx = np.random.default_rng(0).choice(x.size, size=2000, replace=False)
     assert metrics.masked_dc(truth, approx, mask) == np_dc(x[idx], y[idx])
     assert metrics.masked_dc(truth, approx, mask, max_entries=10_000) == np_dc(x, y)
+
+
+def test_b_norm_matches_reference(ops):
+    """tropical.b_norm on the device: the reference's values on 30 arrays up to 200 K
+    elements (tests/golden/ops.npz, bn*_w / bn_sums)."""
+    for t in range(int(ops["n_bn"])):
+        assert pkg.b_norm(ops[f"bn{t}_w"]) == float(ops["bn_sums"][t]), t
+    assert pkg.b_norm(np.zeros((0,))) == 0.0
+
+
+def test_td_helpers(ops):
+    """td_grid (device product) and the single-entry / single-line helpers against the
+    reference's td_grid column sums (ops.npz scores) and direct restatements."""
+    for c in range(0, int(ops["n_ops"]), 2):
+        X, M, U, V = (ops[f"c{c}_{k}"] for k in ("X", "M", "U", "V"))
+        if not M.any(axis=0).all() or not M.any(axis=1).all():
+            continue
+        R = pkg.MaskedMatrix(X, M)
+        grid = pkg.td_grid(R, U, V)
+        assert np.array_equal(grid.sum(axis=0), ops[f"c{c}_scores"]), c
+        gi, gj = np.nonzero(M)
+        i, j = int(gi[0]), int(gj[0])
+        assert pkg.td(R, U, V, i, j) == grid[i, j]
+        assert pkg.argmax_k(U, V, i, j) == int(ops[f"c{c}_arg"][i, j])
+        assert pkg.td_row(R, U, V, i) == float(np.sum(grid[i][M[i]]))
+        assert pkg.td_col(R, U, V, j) == float(np.sum(grid[:, j][M[:, j]]))
