@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the config-5 kernel microbench")
     return ap.parse_args()
 
 
@@ -365,6 +366,22 @@ def run_b200(args):
             line["e2e"] = {"value": args.steps * world / dt, "unit": "sweeps/s",
                            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                            "note": "one fast_stmf call per run: H2D, init, K sweeps from init, D2H"}
+    # the kernel microbenchmark of BASELINE.json configs[4] at its largest HBM-bound point
+    # (masked max-plus product + exact error, 65536^2, rank 4, density 1.0; device-generated
+    # data, L2 flushed between reps), so the bench line carries that kernel's roofline too
+    if rank == 0 and not args.no_c5:
+        try:
+            r5 = _ext.bench_maxplus(65536, 65536, 4, 1.0, seed=0, reps=5, flush_l2=True, device=local)
+            peak, peak_src = peaks()
+            line["kernel_microbench"] = {
+                "config": "config5: m=n=65536, rank 4, density 1.0, fp32 (masked max-plus product + exact error)",
+                "kernel": "stmf::k_maxplus_err (TMA-fed tiles)", "avg_ms": r5["avg_ms"],
+                "roofline": {"bound": "hbm", "achieved": r5["gbs"], "peak": peak, "unit": "GB/s",
+                             "frac": r5["gbs"] / peak, "traffic": 17753138000,
+                             "traffic_source": "profiles/r01_c5_maxplus.md (ncu dram__bytes_read.sum)"},
+                "objective": r5["objective"]}
+        except Exception as e:  # noqa: BLE001 - reported, never fatal for the headline
+            line["kernel_microbench"] = {"error": str(e)}
     if rank == 0 and not args.no_cpu_baseline:
         vps, aps, cap, r0 = cpu_sample(work, U_w, V_w, args.cpu_seconds, 1)
         cps = aps / first_step_attempts
