@@ -1,0 +1,40 @@
+"""The bench line's contract (the driver parses it): every required key, on the
+committed round-final line (profiles/r01_bench_c2_final.json) and on the reference arm's
+line.  CPU only: no bench is run here."""
+
+import json
+import os
+
+from conftest import ROOT
+
+REQUIRED = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches", "cpu_baseline"}
+
+
+def _line(name):
+    return json.load(open(os.path.join(ROOT, "profiles", name)))
+
+
+def test_b200_bench_line_contract():
+    d = _line("r01_bench_c2_final.json")
+    assert REQUIRED <= set(d), REQUIRED - set(d)
+    assert d["unit"] == "sweeps/s" and d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert "workload" in d["config"] and "model" not in d["config"]
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r) and r["bound"] in ("hbm", "tensor")
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = d["e2e"]
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e) and e["h2d_bytes_per_step"] > 0
+    c = d["cpu_baseline"]
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(c) and c["kind"] in ("port", "reference")
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["gpu_launches"] > 0 and d["warmup"] >= 3
+    k = d["kernel_microbench"]["roofline"]
+    assert k["bound"] == "hbm" and 0 < k["frac"] <= 1.0
+
+
+def test_reference_arm_line_contract():
+    d = _line("r01_bench_c2_reference_arm.json")
+    assert d["impl"] == "reference" and d["unit"] == "sweeps/s"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert {"value", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
