@@ -38,3 +38,17 @@ def test_reference_arm_line_contract():
     assert d["impl"] == "reference" and d["unit"] == "sweeps/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert {"value", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+
+
+def test_reference_arm_runs_on_the_host():
+    """`bench.py --impl reference` (the C restatement on the host threads) prints a
+    contract line without any GPU."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--cpu-seconds", "1"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["cores"] >= 1
