@@ -245,3 +245,19 @@ def test_pooled_memory_release_between_fits(fits):
     p2, t2 = pkg.fast_stmf(R, int(c["rank"]), cfg)
     assert np.array_equal(p1.U, p2.U) and np.array_equal(np.array(t1.errors), np.array(t2.errors))
     assert np.array_equal(p1.U, c["U"])
+
+
+def test_config2_sweep1_matches_reference():
+    """BASELINE.json configs[1] itself (500 x 1000, rank 5, fp64, 50% missing): the
+    first sweep against the unmodified reference's fast_stmf (tests/golden/c2sweep1.npz,
+    make_golden_c2sweep1.py) — factors and every trajectory sample bit for bit."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c2sweep1.npz")
+    if not os.path.exists(path):
+        pytest.skip("c2sweep1 fixture not generated")
+    from paper_2205_06619_b200 import gen
+    g = np.load(path)
+    pair, traj = pkg.fast_stmf(gen.config2(), 5, pkg.RunConfig(rank=5, budget_sweeps=1, epsilon=0.0, seed=42))
+    assert np.array_equal(np.array(traj.errors), g["traj_e"])
+    assert np.array_equal(np.array(traj.times), g["traj_t"])
+    assert np.array_equal(pair.U, g["U"]) and np.array_equal(pair.V, g["V"])
