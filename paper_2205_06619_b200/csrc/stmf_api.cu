@@ -1023,7 +1023,7 @@ struct Session : SessionBase {
     int64_t beg = h_row_ptr[i], nc = h_row_ptr[i + 1] - beg;
     if (nc <= 4 * kCandThreads && rank <= 256) {
       auto kern = nc <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
-      kern<<<1, kCandThreads, 0, st>>>((int)nc, n, rank, col_idx.p + beg, xr.p + beg, agr.p + beg, score.p,
+      kern<<<cand_grid(), kCandThreads, 0, st>>>((int)nc, n, rank, col_idx.p + beg, xr.p + beg, agr.p + beg, score.p,
                                        colhist.p, cj.p, ck.p, cx.p, xrow_dense.p, i, cm1.p, cm2.p, cmarg.p, cmi.p,
                                        nullptr, nullptr, selection == STMF_SEL_TD ? 1 : 0);
       LAUNCH_CK();
@@ -1046,6 +1046,12 @@ struct Session : SessionBase {
     row_cmi(i);
     row_partition();
     return nc;
+  }
+
+  // k_cand_row's grid: block 0 ranks the candidates, the others fill CM^(-i)
+  unsigned cand_grid() const {
+    int64_t need = ((int64_t)rank * n + kCandThreads - 1) / kCandThreads;
+    return (unsigned)(1 + std::max<int64_t>(1, std::min<int64_t>(need, nsm)));
   }
 
   // CM^(-i) for the visited row (the statistics are current within a row visit)
@@ -1794,7 +1800,8 @@ struct Session : SessionBase {
     k_g_row_begin<<<1, 1, 0, st>>>(c, row_ptr.p, d_row_depth.p, h_batch, h_acc);
     {
       auto kern = max_rownnz <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
-      kern<<<1, kCandThreads, 0, st>>>(0, n, rank, col_idx.p, xr.p, agr.p, score.p, colhist.p, cj.p, ck.p, cx.p,
+      kern<<<cand_grid(), kCandThreads, 0, st>>>(0, n, rank, col_idx.p, xr.p, agr.p, score.p, colhist.p, cj.p, ck.p,
+                                                 cx.p,
                                        xrow_dense.p, 0, cm1.p, cm2.p, cmarg.p, cmi.p, c, row_ptr.p,
                                        selection == STMF_SEL_TD ? 1 : 0);
     }

@@ -597,8 +597,21 @@ k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const 
   using Sort = cub::BlockMergeSort<u64, kCandThreads, ITEMS, int>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ int32_t rowhist[256];
-  if (g) {  // graph mode: the row from the control block
-    irow = g->i;
+  if (g) irow = g->i;  // graph mode: the row from the control block
+  // CM^(-i) of every k for the visited row (k_cmi): blocks 1.. when the launch has
+  // them (rank * n values), else block 0 itself
+  if (gridDim.x > 1) {
+    if (blockIdx.x > 0) {
+      for (int64_t t = (blockIdx.x - 1) * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rank * n;
+           t += (int64_t)(gridDim.x - 1) * blockDim.x)
+        cmi[t] = (cmarg[t] == (int32_t)irow) ? cm2[t] : cm1[t];
+      return;
+    }
+  } else {
+    for (int64_t t = threadIdx.x; t < (int64_t)rank * n; t += blockDim.x)
+      cmi[t] = (cmarg[t] == (int32_t)irow) ? cm2[t] : cm1[t];
+  }
+  if (g) {
     int64_t beg = row_ptr[irow];
     nc = (int)(row_ptr[irow + 1] - beg);
     cols += beg;
@@ -607,9 +620,6 @@ k_cand_row(int nc, int64_t n, int rank, const int32_t* __restrict__ cols, const 
   }
   for (int l = threadIdx.x; l < rank; l += blockDim.x) rowhist[l] = 0;
   for (int64_t c = threadIdx.x; c < n; c += blockDim.x) xrow_dense[c] = tinf<T>();
-  // CM^(-i) of every k for the visited row (k_cmi)
-  for (int64_t t = threadIdx.x; t < (int64_t)rank * n; t += blockDim.x)
-    cmi[t] = (cmarg[t] == (int32_t)irow) ? cm2[t] : cm1[t];
   __syncthreads();
   u64 key[ITEMS];
   int val[ITEMS];
