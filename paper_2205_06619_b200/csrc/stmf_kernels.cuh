@@ -390,28 +390,28 @@ __global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const i
                            const int* __restrict__ kdev = nullptr) {
   if (kdev) k = *kdev;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
-    {
-      int64_t r = rowof[p], c = colof[p];
-      T b1, b2;
-      int a1, a2;
-      bool full = k < 0;
-      if (!full) {
-        a1 = ag[p];
-        a2 = ag2[p];
-        full = a1 == k || a2 == k;
-      }
-      if (full) {
+    int64_t r = rowof[p], c = colof[p];
+    T b1, b2;
+    int a1, a2;
+    if (k < 0) {
+      top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
+    } else {
+      // every load of the incremental update issued up front (memory-level
+      // parallelism): the cached top-2, their indices and the new k-term
+      a1 = ag[p];
+      a2 = ag2[p];
+      b1 = t1[p];
+      b2 = t2[p];
+      T s = add_rn(Ut[(int64_t)k * m + r], V[(int64_t)k * n + c]);
+      if (a1 == k || a2 == k) {
         top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
       } else {
         // k held neither top-2 slot: insert its new value (lowest index on max ties)
-        T s = add_rn(Ut[(int64_t)k * m + r], V[(int64_t)k * n + c]);
-        b1 = t1[p];
-        b2 = t2[p];
         if (s > b1 || (s == b1 && k < a1)) { b2 = b1; a2 = a1; b1 = s; a1 = k; }
         else if (s > b2) { b2 = s; a2 = k; }
       }
-      t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
     }
+    t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
   }
 }
 
