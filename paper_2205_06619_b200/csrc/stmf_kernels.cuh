@@ -443,10 +443,15 @@ k_scores(int64_t n, int rank, const int64_t* __restrict__ ptr, const T* __restri
     for (int64_t base = beg; base < end; base += 32) {
       int64_t p = base + lane;
       double td = 0.0;
+      int a = -1;
       if (p < end) {
         td = (double)vabs(sub_rn(xc[p], t1[p]));
-        atomicAdd(&hist[wib][ag[p]], 1);
+        a = ag[p];
       }
+      // warp-aggregated histogram: one lane per distinct argmax adds its peers' count
+      // (leaders hold distinct bins, so plain shared-memory adds do not race)
+      unsigned peers = __match_any_sync(0xffffffffu, a);
+      if (a >= 0 && lane == __ffs(peers) - 1) hist[wib][a] += __popc(peers);
       if (seq) {
         int cnt = end - base < 32 ? (int)(end - base) : 32;
         for (int l = 0; l < cnt; l++) s = __dadd_rn(s, __shfl_sync(0xffffffffu, td, l));
