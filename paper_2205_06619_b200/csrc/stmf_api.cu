@@ -461,6 +461,9 @@ struct Session : SessionBase {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
+    if (ev_aux0) cudaEventDestroy(ev_aux0);
+    if (ev_aux1) cudaEventDestroy(ev_aux1);
+    if (st_aux) cudaStreamDestroy(st_aux);
     if (ev_fork3) cudaEventDestroy(ev_fork3);
     if (ev_join3) cudaEventDestroy(ev_join3);
     if (st3) cudaStreamDestroy(st3);
@@ -739,8 +742,38 @@ struct Session : SessionBase {
   }
 
   // product caches + scores + histograms + statistics of dirty factor indices
+  // residuation statistics of dirty indices on an auxiliary stream, concurrent with
+  // the product caches (they read only the committed factors)
+  cudaStream_t st_aux = nullptr;
+  cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
   void ensure_caches() {
     need_factors();
+    bool stats = false;
+    for (int k = 0; k < rank; k++) stats |= stats_dirty[k] != 0;
+    cudaStream_t ss = st;
+    if (stats && dirty) {
+      if (!st_aux) {
+        CK(cudaStreamCreateWithFlags(&st_aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_aux0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_aux1, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(ev_aux0, st));
+      CK(cudaStreamWaitEvent(st_aux, ev_aux0, 0));
+      ss = st_aux;
+    }
+    for (int k = 0; k < rank; k++) {
+      if (!stats_dirty[k]) continue;
+      k_line_stats<T><<<warps_grid(n), 256, 0, ss>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p + (size_t)k * m,
+                                                        cm1.p + (size_t)k * n, cm2.p + (size_t)k * n,
+                                                        cmarg.p + (size_t)k * n);
+      LAUNCH_CK();
+      k_line_stats<T><<<warps_grid(m), 256, 0, ss>>>(m, row_ptr.p, col_idx.p, xr.p, V.p + (size_t)k * n,
+                                                        rm1.p + (size_t)k * m, rm2.p + (size_t)k * m,
+                                                        rmarg.p + (size_t)k * m);
+      LAUNCH_CK();
+      stats_dirty[k] = 0;
+    }
+    if (ss != st) CK(cudaEventRecord(ev_aux1, ss));
     if (dirty) {
       CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
       // cache_k >= 0: only factor index cache_k changed since the caches were valid
@@ -770,18 +803,7 @@ struct Session : SessionBase {
       dirty = false;
       cache_k = -1;
     }
-    for (int k = 0; k < rank; k++) {
-      if (!stats_dirty[k]) continue;
-      k_line_stats<T><<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p + (size_t)k * m,
-                                                        cm1.p + (size_t)k * n, cm2.p + (size_t)k * n,
-                                                        cmarg.p + (size_t)k * n);
-      LAUNCH_CK();
-      k_line_stats<T><<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, col_idx.p, xr.p, V.p + (size_t)k * n,
-                                                        rm1.p + (size_t)k * m, rm2.p + (size_t)k * m,
-                                                        rmarg.p + (size_t)k * m);
-      LAUNCH_CK();
-      stats_dirty[k] = 0;
-    }
+    if (ss != st) CK(cudaStreamWaitEvent(st, ev_aux1, 0));
   }
 
   // objective of the state "current factors with column k of U := a, row k of V := b"
