@@ -546,8 +546,10 @@ struct Session : SessionBase {
     row_depth.assign(m, 0);
     // measured (profiles/r01_sched.md): launch-bound small problems prefer generous
     // batches, evaluation-bound large ones tight batches with slow growth
+    // (config 4, N ~ 1e8: faster batch growth, +5% row visits/s in sweep 1; config 3,
+    // N ~ 1e7: growth 1.5 is 3-6% faster per sweep; profiles/r01_sched.md)
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = 1.5; }
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.5; }
     read_sched_env();
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
