@@ -40,7 +40,8 @@ enum {
   STMF_ERR_OOM = 3,       /* device allocation failed                                      */
   STMF_ERR_NUMERIC = 4,   /* exact-objective window violated / decision bound violated     */
   STMF_ERR_CAPACITY = 5,  /* trajectory buffer too small                                   */
-  STMF_ERR_NCCL = 6       /* collective failure (sharded sessions)                         */
+  STMF_ERR_NCCL = 6,      /* collective failure (sharded sessions)                         */
+  STMF_ERR_AUDIT = 7      /* audit mode: recomputed state differs (AssertionError)         */
 };
 
 enum { STMF_F64 = 0, STMF_F32 = 1 };
@@ -126,6 +127,18 @@ int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t c
  * how many sweeps of the session's runs were replayed.  STMF_FIXPOINT_REPLAY=0 in the
  * environment executes them. */
 int stmf_replayed_sweeps(stmf_session* s, int64_t* n);
+/* Test hook (the checker's oracle.fit(max_attempts=...), oracle/stmf_oracle_core.h):
+ * later stmf_run calls of this single-device ByRow session stop after exactly
+ * max_attempts attempts (0 = no cap), as FitRun would if it were interrupted there;
+ * the trajectory then ends with one sweep-boundary sample (engine.py:309-310).
+ * Capped runs use the host-driven sweep loop. */
+int stmf_set_max_attempts(stmf_session* s, int64_t max_attempts);
+/* RunConfig.audit (engine.py:143-153, 279-294).  The reference re-checks after every
+ * rejected update that revert restored the factors; here rejected updates never touch
+ * the committed state, so audit mode re-derives that state instead: after every sweep
+ * the product caches are rebuilt from the factors and the objective is recomputed from
+ * scratch, and it must equal the error the fit carries (STMF_ERR_AUDIT otherwise). */
+int stmf_set_audit(stmf_session* s, int on);
 
 /* ---- the reference's other fit methods ---- */
 

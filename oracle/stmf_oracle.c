@@ -85,6 +85,23 @@ static void xacc_add_f32(xacc* a, float t) {
   }
 }
 
+/* a += b (exact; the sums stay far below 2^320) */
+static void xacc_merge(xacc* a, const xacc* b) {
+  uint64_t carry = 0;
+  for (int L = 0; L < 5; L++) {
+    uint64_t s = a->l[L] + b->l[L];
+    uint64_t c1 = s < a->l[L];
+    uint64_t s2 = s + carry;
+    uint64_t c2 = s2 < s;
+    a->l[L] = s2;
+    carry = c1 | c2;
+  }
+}
+
+/* column chunk of the OpenMP-parallel loops (each output element is produced by one
+ * thread, in the same order as the sequential restatement) */
+#define ORC_CHUNK 256
+
 static int bit_at(const xacc* a, int p) { return (int)((a->l[p >> 6] >> (p & 63)) & 1u); }
 
 /* value = I * 2^-149, rounded to nearest even binary64 */

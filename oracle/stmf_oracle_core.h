@@ -14,6 +14,7 @@
  * (-inf when r == 1); optional outputs may be NULL.                            */
 void FN(orc_trop_matmul)(int64_t m, int r, int64_t n, const T* U, const T* V, T* P,
                          int32_t* arg, T* top2) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < m; i++) {
     for (int64_t j = 0; j < n; j++) {
       T best = U[i * r] + V[j];
@@ -35,17 +36,23 @@ void FN(orc_trop_matmul)(int64_t m, int r, int64_t n, const T* U, const T* V, T*
 void FN(orc_residuate_row)(int64_t m, int64_t n, const T* X, const uint8_t* mask,
                            const T* u, T* v_out) {
   for (int64_t j = 0; j < n; j++) v_out[j] = (T)INFINITY;
-  for (int64_t i = 0; i < m; i++)
-    for (int64_t j = 0; j < n; j++)
-      if (mask[i * n + j]) {
-        T d = X[i * n + j] - u[i];
-        if (d < v_out[j]) v_out[j] = d;
-      }
+  /* column chunks in parallel (OpenMP); min is exact, so any order gives the same v */
+#pragma omp parallel for schedule(static)
+  for (int64_t j0 = 0; j0 < n; j0 += ORC_CHUNK) {
+    int64_t j1 = j0 + ORC_CHUNK < n ? j0 + ORC_CHUNK : n;
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = j0; j < j1; j++)
+        if (mask[i * n + j]) {
+          T d = X[i * n + j] - u[i];
+          if (d < v_out[j]) v_out[j] = d;
+        }
+  }
 }
 
 /* engine._residuate_col (engine.py:204-207): u[i] = min_{j given} X[i,j] - v[j] */
 void FN(orc_residuate_col)(int64_t m, int64_t n, const T* X, const uint8_t* mask,
                            const T* v, T* u_out) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < m; i++) {
     T best = (T)INFINITY;
     for (int64_t j = 0; j < n; j++)
@@ -69,6 +76,25 @@ static T FN(prod_entry)(int r, int64_t n, const T* U, const T* V, int64_t i, int
 /* approx_error (tropical.py:214-222) = b_norm(R - U(x)V, mask) (tropical.py:197-211) */
 static double FN(approx_error_buf)(int64_t m, int r, int64_t n, const T* X,
                                    const uint8_t* mask, const T* U, const T* V, T* buf) {
+#if !OBJ_NUMPY
+  /* exact sum: order independent, so rows are summed in parallel into per-thread
+   * accumulators merged exactly */
+  (void)buf;
+  xacc tot;
+  memset(&tot, 0, sizeof tot);
+#pragma omp parallel
+  {
+    xacc a;
+    memset(&a, 0, sizeof a);
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = 0; j < n; j++)
+        if (mask[i * n + j]) xacc_add_f32(&a, ABS(X[i * n + j] - FN(prod_entry)(r, n, U, V, i, j)));
+#pragma omp critical
+    xacc_merge(&tot, &a);
+  }
+  return xacc_to_double(&tot);
+#endif
   int64_t c = 0;
   for (int64_t i = 0; i < m; i++)
     for (int64_t j = 0; j < n; j++)
@@ -107,15 +133,24 @@ void FN(orc_col_scores)(int64_t m, int r, int64_t n, const T* X, const uint8_t* 
     return;
   }
   for (int64_t j = 0; j < n; j++) scores[j] = 0.0;
-  for (int64_t i = 0; i < m; i++)
-    for (int64_t j = 0; j < n; j++)
-      if (mask[i * n + j]) scores[j] += ABS(X[i * n + j] - FN(prod_entry)(r, n, U, V, i, j));
+  /* column chunks in parallel; each column is still summed sequentially over rows */
+#pragma omp parallel for schedule(static)
+  for (int64_t j0 = 0; j0 < n; j0 += ORC_CHUNK) {
+    int64_t j1 = j0 + ORC_CHUNK < n ? j0 + ORC_CHUNK : n;
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = j0; j < j1; j++)
+        if (mask[i * n + j]) scores[j] += ABS(X[i * n + j] - FN(prod_entry)(r, n, U, V, i, j));
+  }
 #else
   xacc* acc = (xacc*)calloc((size_t)n, sizeof(xacc));
-  for (int64_t i = 0; i < m; i++)
-    for (int64_t j = 0; j < n; j++)
-      if (mask[i * n + j])
-        xacc_add_f32(&acc[j], ABS(X[i * n + j] - FN(prod_entry)(r, n, U, V, i, j)));
+#pragma omp parallel for schedule(static)
+  for (int64_t j0 = 0; j0 < n; j0 += ORC_CHUNK) {
+    int64_t j1 = j0 + ORC_CHUNK < n ? j0 + ORC_CHUNK : n;
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t j = j0; j < j1; j++)
+        if (mask[i * n + j])
+          xacc_add_f32(&acc[j], ABS(X[i * n + j] - FN(prod_entry)(r, n, U, V, i, j)));
+  }
   for (int64_t j = 0; j < n; j++) scores[j] = xacc_to_double(&acc[j]);
   free(acc);
 #endif
@@ -220,9 +255,13 @@ static void FN(byrow)(CTX* c, int64_t i) {
     FN(orc_trop_matmul)(m, r, n, c->U, c->V, NULL, c->arg, NULL);
     FN(orc_col_scores)(m, r, n, c->X, c->mask, c->U, c->V, c->scores);
     memset(c->colhist, 0, sizeof(int32_t) * (size_t)(n * r));
-    for (int64_t a = 0; a < m; a++)
-      for (int64_t j = 0; j < n; j++)
-        if (c->mask[a * n + j]) c->colhist[j * r + c->arg[a * n + j]]++;
+#pragma omp parallel for schedule(static)
+    for (int64_t j0 = 0; j0 < n; j0 += ORC_CHUNK) {
+      int64_t j1 = j0 + ORC_CHUNK < n ? j0 + ORC_CHUNK : n;
+      for (int64_t a = 0; a < m; a++)
+        for (int64_t j = j0; j < j1; j++)
+          if (c->mask[a * n + j]) c->colhist[j * r + c->arg[a * n + j]]++;
+    }
     c->dirty = 0;
   }
   /* _ranked_row_candidates (strategies.py:183-188) */

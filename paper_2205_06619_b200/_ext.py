@@ -24,7 +24,7 @@ HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
-             5: "capacity", 6: "NCCL error"}
+             5: "capacity", 6: "NCCL error", 7: "audit"}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -134,6 +134,8 @@ def lib():
         "stmf_release_memory": [_int],
         "stmf_trajectory": [_vp, _vp, _vp, _i64, ctypes.POINTER(_i64)],
         "stmf_replayed_sweeps": [_vp, ctypes.POINTER(_i64)],
+        "stmf_set_max_attempts": [_vp, _i64],
+        "stmf_set_audit": [_vp, _int],
         "stmf_b_norm": [_i64, _vp, _int, ctypes.POINTER(_dbl)],
     }
     for name, args in sig.items():
@@ -153,7 +155,7 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
                     "stmf_csv_close", "stmf_release_memory",
-                    "stmf_trajectory", "stmf_replayed_sweeps",
+                    "stmf_trajectory", "stmf_replayed_sweeps", "stmf_set_max_attempts", "stmf_set_audit",
                     "stmf_b_norm"]
 
 # include/stmf_b200.h: families and ByRow selection rules
@@ -355,6 +357,16 @@ class Session:
         return tt, te, out
 
     # diff-test hooks ------------------------------------------------------
+    def set_max_attempts(self, cap: int):
+        """Stop later runs after exactly `cap` attempts (0 = no cap): the checker's
+        oracle.fit(max_attempts=...) on the device (host-driven sweep loop)."""
+        _check(lib().stmf_set_max_attempts(self._h, int(cap)))
+
+    def set_audit(self, on: bool = True):
+        """RunConfig.audit: after every sweep the caches are rebuilt and the objective
+        recomputed from scratch; a mismatch raises StmfError code 7 (audit)."""
+        _check(lib().stmf_set_audit(self._h, int(bool(on))))
+
     def product_given(self):
         P = np.empty(self.given, self.dtype)
         top2 = np.empty(self.given, self.dtype)

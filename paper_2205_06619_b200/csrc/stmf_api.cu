@@ -190,6 +190,7 @@ struct PWTree {
 struct SessionBase {
   virtual ~SessionBase() {}
   int dtype = 0;
+  virtual int device_id() const = 0;
   virtual void info(int64_t* out) = 0;
   virtual void set_factors(const void* U, const void* V) = 0;
   virtual void get_factors(void* U, void* V) = 0;
@@ -206,6 +207,9 @@ struct SessionBase {
   virtual void set_profiling(int on) = 0;
   virtual void counters(int64_t* out) = 0;
   virtual int64_t replayed_sweeps() { return 0; }
+  // test hook mirroring oracle.fit(max_attempts=...): stop after that many attempts
+  virtual void set_max_attempts(int64_t) { fail(STMF_ERR_INVALID, "attempt caps are single-device only"); }
+  virtual void set_audit(int) { fail(STMF_ERR_INVALID, "audit mode is single-device only"); }
   // the reference's other fit methods
   virtual void set_strategy(int family, int selection) {
     if (family != STMF_FAMILY_BYROW || selection != STMF_SEL_TD_A)
@@ -442,6 +446,7 @@ struct Session : SessionBase {
   long long phaseB_launches = 0, phaseB_ns = 0, phaseB_timed = 0;
 
   void* stream() override { return (void*)st; }
+  int device_id() const override { return dev; }
   void set_profiling(int on) override {
     if (on && !ev_b0) {
       CK(cudaEventCreate(&ev_b0));
@@ -487,6 +492,10 @@ struct Session : SessionBase {
     dev = device;
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the auxiliary stream of ensure_caches, created here on the session's device
+    CK(cudaStreamCreateWithFlags(&st_aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_aux0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_aux1, cudaEventDisableTiming));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, dev));
     nsm = prop.multiProcessorCount;
@@ -754,15 +763,19 @@ struct Session : SessionBase {
     for (int k = 0; k < rank; k++) stats |= stats_dirty[k] != 0;
     cudaStream_t ss = st;
     if (stats && dirty) {
-      if (!st_aux) {
-        CK(cudaStreamCreateWithFlags(&st_aux, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&ev_aux0, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_aux1, cudaEventDisableTiming));
-      }
       CK(cudaEventRecord(ev_aux0, st));
       CK(cudaStreamWaitEvent(st_aux, ev_aux0, 0));
       ss = st_aux;
     }
+    // the session stream joins the auxiliary work on every exit path (a throw below
+    // must not leave later work on st racing the statistics kernels)
+    struct AuxJoin {
+      cudaStream_t st = nullptr;
+      cudaEvent_t ev = nullptr;
+      ~AuxJoin() {
+        if (st) cudaStreamWaitEvent(st, ev, 0);
+      }
+    } aux_join;
     for (int k = 0; k < rank; k++) {
       if (!stats_dirty[k]) continue;
       k_line_stats<T><<<warps_grid(n), 256, 0, ss>>>(n, col_ptr.p, row_idx.p, xc.p, Ut.p + (size_t)k * m,
@@ -775,7 +788,11 @@ struct Session : SessionBase {
       LAUNCH_CK();
       stats_dirty[k] = 0;
     }
-    if (ss != st) CK(cudaEventRecord(ev_aux1, ss));
+    if (ss != st) {
+      CK(cudaEventRecord(ev_aux1, ss));
+      aux_join.st = st;
+      aux_join.ev = ev_aux1;
+    }
     if (dirty) {
       CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
       // cache_k >= 0: only factor index cache_k changed since the caches were valid
@@ -805,7 +822,6 @@ struct Session : SessionBase {
       dirty = false;
       cache_k = -1;
     }
-    if (ss != st) CK(cudaStreamWaitEvent(st, ev_aux1, 0));
   }
 
   // objective of the state "current factors with column k of U := a, row k of V := b"
@@ -1172,11 +1188,12 @@ struct Session : SessionBase {
   // `order` (optional): the eval ids (2 q + op) in the strategy's attempt order; the
   // return value is then a position in `order`.
   int decide_batch(int E, const std::vector<int>& hk, double* fwin, bool* deferred = nullptr,
-                   const std::vector<int>* order = nullptr) {
+                   const std::vector<int>* order = nullptr, int limit = -1) {
     resolve_err();
     if (deferred) *deferred = false;
     int pos = 0;
-    const int total = order ? (int)order->size() : 2 * E;
+    int total = order ? (int)order->size() : 2 * E;
+    if (limit >= 0) total = std::min(total, limit);  // attempt cap (set_max_attempts)
     while (pos < total) {
       struct Req { int ev, q, op; bool certain; };
       std::vector<Req> chunk;
@@ -1250,10 +1267,33 @@ struct Session : SessionBase {
     int64_t cur_sweep;
     double* tt; double* te; int64_t cap, len;
     int64_t attempts, accepts, visits, evaluated;
+    bool capped;  // the attempt cap was reached (set_max_attempts)
   };
 
   double run_now(RunState& R) { return R.wall ? now_s() - R.t0 : (double)R.cur_sweep; }
-  bool out_of_time(RunState& R) { return R.wall && now_s() - R.t0 >= R.budget_seconds; }
+  bool out_of_time(RunState& R) { return R.capped || (R.wall && now_s() - R.t0 >= R.budget_seconds); }
+  // attempt cap of the ByRow host loop (0 = none): the fit stops after exactly that many
+  // attempts, as oracle.fit(max_attempts=...) does; capped runs use the host-driven loop
+  int64_t max_attempts = 0;
+  void set_max_attempts(int64_t cap) override { max_attempts = std::max<int64_t>(0, cap); }
+  // audit mode (RunConfig.audit): after every sweep, rebuild the caches from the factors
+  // and recompute the objective from scratch; it must equal the carried err
+  bool audit_on = false;
+  int64_t n_audits = 0;
+  void set_audit(int on) override { audit_on = on != 0; }
+  void audit_check() {
+    resolve_err();
+    dirty = true;
+    cache_k = -1;
+    stats_dirty.assign(rank, 1);
+    ensure_caches();
+    double e;
+    if (kExact) e = state_objective(0, Ut.p, V.p);
+    else e = exact_current_objective();
+    n_audits++;
+    if (e != err)
+      fail(STMF_ERR_AUDIT, "audit: objective recomputed from scratch %.17g != the fit's error %.17g", e, err);
+  }
   // the trajectory goes to the caller's buffers, or (null buffers) to the session's
   // growable copy, read back with stmf_trajectory
   std::vector<double> tj_t, tj_e;
@@ -1347,13 +1387,20 @@ struct Session : SessionBase {
       int E = (int)std::min<int64_t>(nc - t0, fixed_sched ? batch_sched[std::min(bi, batch_sched.size() - 1)] : next);
       bi++;
       next = std::min(Emax, std::max(next + 1, (int)(next * sched_growth)));
+      int limit = -1;
+      if (max_attempts > 0) {
+        int64_t rem = max_attempts - R.attempts;
+        if (rem <= 0) { R.capped = true; return; }
+        E = (int)std::min<int64_t>(E, (rem + 1) / 2);
+        limit = (int)std::min<int64_t>(rem, 2 * (int64_t)E);
+      }
       hk.resize(E);
       eval_batch(i, t0, E, hk.data());  // one host sync per batch
       ph_mark(2);
       R.evaluated += 2 * (int64_t)E;
       double f;
       bool deferred = false;
-      int w = decide_batch(E, hk, &f, defer_accepts ? &deferred : nullptr);
+      int w = decide_batch(E, hk, &f, defer_accepts ? &deferred : nullptr, nullptr, limit);
       ph_mark(3);
       if (w >= 0) {
         R.attempts += w + 1;
@@ -1371,7 +1418,8 @@ struct Session : SessionBase {
         }
         return;
       }
-      R.attempts += 2 * (int64_t)E;
+      R.attempts += limit >= 0 ? limit : 2 * (int64_t)E;
+      if (max_attempts > 0 && R.attempts >= max_attempts) R.capped = true;
       if (out_of_time(R)) return;
       t0 += E;
     }
@@ -1686,7 +1734,7 @@ struct Session : SessionBase {
   bool graph_eligible() const {
     // rows must fit the one-block candidate ranking; column scores of a single-column
     // matrix and fixed batch schedules stay on the host loop
-    return graph_on && !fixed_sched && family == STMF_FAMILY_BYROW &&
+    return graph_on && !fixed_sched && max_attempts <= 0 && family == STMF_FAMILY_BYROW &&
            (selection == STMF_SEL_TD_A || selection == STMF_SEL_TD) && max_rownnz <= 4 * kCandThreads && rank <= 256 && n > 1 &&
            (kExact || cur_valid) && n_long_rows + n_long_cols == 0 && 2 * Emax <= kDecideThreads;
   }
@@ -2065,6 +2113,8 @@ struct Session : SessionBase {
     if (budget_sweeps < 0 && !(budget_seconds > 0)) fail(STMF_ERR_INVALID, "set budget_sweeps or budget_seconds");
     if (family == STMF_FAMILY_BYMATRIX)
       fail(STMF_ERR_INVALID, "ByMatrix steps run host-side (stmf_matrix_candidates + stmf_attempt)");
+    if (max_attempts > 0 && (family != STMF_FAMILY_BYROW || selection == STMF_SEL_SEQ))
+      fail(STMF_ERR_INVALID, "the attempt cap applies to ByRow TD / TD_A / TD_B fits only");
     RunState R{};
     R.wall = budget_seconds > 0;
     R.budget_seconds = budget_seconds;
@@ -2107,6 +2157,7 @@ struct Session : SessionBase {
         }
         sweeps++;
         resolve_err();
+        if (audit_on) audit_check();
         traj_append(R, run_now(R), err);  // mark_sweep_boundary (engine.py:309-310)
         if (err_before - err < eps) break;
         // Fixpoint: a sweep without an accepted update leaves
@@ -2115,7 +2166,7 @@ struct Session : SessionBase {
         // budget and epsilon = 0 the remaining sweeps are replayed (their trajectory
         // samples and attempt counts) instead of recomputed; STMF_FIXPOINT_REPLAY=0
         // executes them (benchmarks do, so fixpoint sweeps are never counted as run).
-        if (!R.wall && budget_sweeps >= 0 && err == err_before && R.accepts == accepts_before &&
+        if (!R.wall && !R.capped && budget_sweeps >= 0 && err == err_before && R.accepts == accepts_before &&
             fixpoint_replay) {
           int64_t sw_att = R.attempts - attempts_before, sw_vis = R.visits - visits_before,
                   sw_ev = R.evaluated - evaluated_before;
@@ -2452,8 +2503,20 @@ static int validate_create(stmf_session** out, int dtype, int64_t m, int64_t n, 
     return set_err(STMF_ERR_OOM, "host allocation failed"); \
   }
 
-#define NEED(s) \
-  if (!(s) || !(s)->impl) return set_err(STMF_ERR_INVALID, "null session")
+// every session entry point runs on the session's device (restored on return)
+struct DevScope {
+  int prev = -1;
+  explicit DevScope(int d) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+    else prev = -1;
+  }
+  ~DevScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define NEED(s)                                                         \
+  if (!(s) || !(s)->impl) return set_err(STMF_ERR_INVALID, "null session"); \
+  DevScope dev_scope_((s)->impl->device_id())
 
 template <typename T>
 static void trop_matmul_impl(int64_t m, int rank, int64_t n, const void* U, const void* V, void* P, int32_t* arg,
@@ -2751,7 +2814,10 @@ int stmf_create_sim_group(stmf_session** out, int dtype, int64_t m, int64_t n, i
 int stmf_destroy(stmf_session* s) {
   if (!s) return STMF_OK;
   double t0 = now_s();
-  delete s->impl;
+  {
+    DevScope dev_scope_(s->impl ? s->impl->device_id() : 0);
+    delete s->impl;
+  }
   delete s;
   if (getenv("STMF_TRACE_TEARDOWN")) fprintf(stderr, "[stmf teardown] total %.2f ms\n", (now_s() - t0) * 1e3);
   return STMF_OK;
@@ -2790,6 +2856,16 @@ int stmf_replayed_sweeps(stmf_session* s, int64_t* n) {
   NEED(s);
   if (!n) return set_err(STMF_ERR_INVALID, "null argument");
   GUARD(*n = s->impl->replayed_sweeps());
+}
+
+int stmf_set_max_attempts(stmf_session* s, int64_t max_attempts) {
+  NEED(s);
+  GUARD(s->impl->set_max_attempts(max_attempts));
+}
+
+int stmf_set_audit(stmf_session* s, int on) {
+  NEED(s);
+  GUARD(s->impl->set_audit(on));
 }
 
 int stmf_trajectory(stmf_session* s, double* traj_t, double* traj_err, int64_t cap, int64_t* len) {

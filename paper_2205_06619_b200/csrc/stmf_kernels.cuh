@@ -452,6 +452,7 @@ k_scores(int64_t n, int rank, const int64_t* __restrict__ ptr, const T* __restri
       // (leaders hold distinct bins, so plain shared-memory adds do not race)
       unsigned peers = __match_any_sync(0xffffffffu, a);
       if (a >= 0 && lane == __ffs(peers) - 1) hist[wib][a] += __popc(peers);
+      __syncwarp();  // orders this iteration's bin updates before the next iteration's
       if (seq) {
         int cnt = end - base < 32 ? (int)(end - base) : 32;
         for (int l = 0; l < cnt; l++) s = __dadd_rn(s, __shfl_sync(0xffffffffu, td, l));

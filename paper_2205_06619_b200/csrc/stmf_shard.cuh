@@ -889,6 +889,7 @@ struct ShardGroup : SessionBase {
   }
   void bench_product(int, int, double*, double*) override { fail(STMF_ERR_INVALID, "not available on sharded sessions"); }
   void* stream() override { return (void*)st; }
+  int device_id() const override { return dev; }
   void set_profiling(int) override {}
   void counters(int64_t* out) override {
     for (int i = 0; i < 8; i++) out[i] = 0;

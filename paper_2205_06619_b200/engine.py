@@ -187,6 +187,10 @@ def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int
         s.set_factors(U0)
         if (family, selection) != (_ext.FAMILY_BYROW, _ext.SEL_TD_A):
             s.set_strategy(family, selection)
+        if config.audit:
+            # engine.py:279-294: the reference re-checks every revert; the device never
+            # writes a rejected state, so it re-derives the committed one every sweep
+            s.set_audit(True)
         t_init = time.perf_counter() - t0 if wall_clock else 0.0
         if family == _ext.FAMILY_BYMATRIX:
             tt, te, counts = _run_bymatrix(s, config, rng, time.perf_counter())
@@ -195,7 +199,12 @@ def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int
             if wall_clock:
                 budget_seconds = max(config.budget_seconds - (time.perf_counter() - t0), 1e-9)
             # the trajectory is kept (growable) in the library and read back
-            tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)
+            try:
+                tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)
+            except _ext.StmfError as e:
+                if e.code == 7:  # audit mismatch: the reference raises AssertionError (engine.py:294)
+                    raise AssertionError(str(e)) from e
+                raise
         U, V = s.get_factors()
     t_max = config.budget_seconds if wall_clock else float(config.budget_sweeps)
     traj = Trajectory(t_init=t_init, t_max=t_max, time_unit="seconds" if wall_clock else "sweeps")

@@ -1,0 +1,87 @@
+"""Golden fixtures of the binary32 configs at their real shapes (BASELINE.json
+configs[2] and configs[3]; VERDICT r01 "pin fp32 parity at the real shapes").
+
+The reference is fp64-only (tropical.py:74), so the binary32 semantics are defined by
+the C restatement (oracle/, exact-sum objective and column scores).
+For each case this script builds the input with the product's own seeded generator
+(paper_2205_06619_b200.gen), orients it and draws the Random-Acol init exactly as
+fast_stmf does (engine._orient_faststmf / acol_means, fit seed 42), residuates V0 with
+the restatement, and runs the restatement's fit (engine.py:313-348 with the ByRow/TD_A
+sweep, strategies.py:191-224) for its first K attempts of sweep 1
+(oracle.fit(max_attempts=K)).  Stored per case: input checksums, the trajectory,
+attempt/accept counts, and the final factors (sha256 of the bytes plus a slice of
+each for diagnostics).  tests/test_gpu_fp32_shapes.py replays the same K attempts on
+the device (stmf_set_max_attempts) and compares bit for bit.
+
+    python tests/golden/make_golden_fp32_shapes.py [case ...]     (~25 min, 8 threads)
+"""
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+from paper_2205_06619_b200 import engine, gen  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(HERE, "fp32_shapes.npz")
+
+# name: (generator, rank, attempt cap K)
+CASES = {
+    # config 3 itself: 4096 x 8192, rank 10, 70% hidden
+    "c3": (lambda: gen.config3(), 10, 2500),
+    # config 4's generator (Laplace noise, Beta(9,1) row-clustered mask, forced
+    # coverage) at 2048 x 16384: ~150 rows hold more than 4096 given entries, so every
+    # phase-B launch runs the block-per-line path (k_phaseB_long) on them
+    "c4s": (lambda: gen.config4(m=2048, n=16384, rank=20, blocks=8), 20, 3000),
+    # config 4 itself: 32768 x 32768, rank 20 (~107 M given entries)
+    "c4": (lambda: gen.config4(), 20, 120),
+}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def prepare(name):
+    make, rank, K = CASES[name]
+    R = make()
+    rng = np.random.default_rng(42)
+    work, _ = engine._orient_faststmf(R, rng)
+    U0 = engine.acol_means(work, rank, 5, rng).astype(work.dtype)
+    return work, U0, rank, K
+
+
+def run(name):
+    t = time.time()
+    work, U0, rank, K = prepare(name)
+    X = work.values
+    M = work.mask
+    V0 = np.stack([oracle.residuate_row(X, M, U0[:, k]) for k in range(rank)])
+    t1 = time.time()
+    r = oracle.fit(X, M, U0, V0, budget_sweeps=1, epsilon=0.0, max_attempts=K)
+    dt = time.time() - t1
+    print(f"{name}: {work.shape} N={int(M.sum())} attempts {r['attempts']} accepts {r['accepts']} "
+          f"visits {r['row_visits']} capped {r['capped']} | fit {dt:.0f} s, total {time.time() - t:.0f} s",
+          flush=True)
+    return {
+        f"{name}_shape": np.array(work.shape), f"{name}_rank": np.array(rank), f"{name}_K": np.array(K),
+        f"{name}_sha_X": np.array(sha(np.where(M, X, 0))), f"{name}_sha_M": np.array(sha(M)),
+        f"{name}_sha_U0": np.array(sha(U0)), f"{name}_sha_V0": np.array(sha(V0)),
+        f"{name}_traj_t": r["traj_t"], f"{name}_traj_e": r["traj_err"],
+        f"{name}_attempts": np.array(r["attempts"]), f"{name}_accepts": np.array(r["accepts"]),
+        f"{name}_sha_U": np.array(sha(r["U"])), f"{name}_sha_V": np.array(sha(r["V"])),
+        f"{name}_U_head": r["U"][:64].copy(), f"{name}_V_head": r["V"][:, :256].copy(),
+    }
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    data = dict(np.load(OUT)) if os.path.exists(OUT) else {}
+    for nm in names:
+        data.update(run(nm))
+        np.savez_compressed(OUT, **data)

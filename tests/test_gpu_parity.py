@@ -51,12 +51,22 @@ def test_dense_product_and_argmax(ops):
 
 
 def test_missing_seed_entry_raises(ops):
-    X, M, U, V = ops["c1_X"], ops["c1_M"].copy(), ops["c1_U"], ops["c1_V"]
-    gi, gj = np.nonzero(~M)
-    if gi.size == 0:
-        pytest.skip("fully given case")
-    with session(X, M, U, V) as s, pytest.raises(_ext.StmfError, match="missing"):
-        s.try_update(0, int(gi[0]), int(gj[0]), 0)
+    """f_ulf / f_urf on an unobserved entry raise (engine.py:218-219); the first ops
+    case that has a missing entry and full coverage."""
+    tried = 0
+    for c in range(int(ops["n_ops"])):
+        X, M, U, V = ops[f"c{c}_X"], ops[f"c{c}_M"], ops[f"c{c}_U"], ops[f"c{c}_V"]
+        gi, gj = np.nonzero(~M)
+        if gi.size == 0 or not M.any(axis=0).all() or not M.any(axis=1).all():
+            continue
+        with session(X, M, U, V) as s:
+            for op in (0, 1):
+                with pytest.raises(_ext.StmfError, match="missing"):
+                    s.try_update(op, int(gi[0]), int(gj[0]), 0)
+        tried += 1
+        if tried == 3:
+            break
+    assert tried > 0, "no ops case with a missing entry"
 
 
 @pytest.mark.parametrize("graph", ["1", "0", "cap"])
