@@ -78,7 +78,8 @@ int stmf_destroy(stmf_session* s);
  * ((row_starts[shard+1]-row_starts[shard]) x n), the global per-row given counts
  * row_nnz (m values) and the same NCCL unique id (from stmf_nccl_unique_id on one
  * rank, distributed by the caller).  Factor calls then take/return the caller's
- * rows of U and the full V.
+ * rows of U and the full V.  nccl_id may be NULL only for world == 1 (a local
+ * group without NCCL); with an id, world == 1 runs a single-rank NCCL communicator.
  */
 int stmf_nccl_unique_id(void* out, int64_t* bytes);
 int stmf_create_sharded(stmf_session** out, int dtype, int64_t m, int64_t n, int rank,

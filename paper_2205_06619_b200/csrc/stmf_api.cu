@@ -2765,7 +2765,9 @@ int stmf_create_sharded(stmf_session** out, int dtype, int64_t m, int64_t n, int
     for (int s = 0; s < world; s++)
       if (starts[s + 1] <= starts[s]) fail(STMF_ERR_INVALID, "empty shard %d", s);
     CK(cudaSetDevice(device));
-    Comm* c = world > 1 ? (Comm*)new NcclComm(world, shard, nccl_id) : (Comm*)new LocalComm(1);
+    // an NCCL communicator whenever an id is given (world 1 included: the single-rank
+    // communicator runs the same collective calls), else the trivial local group
+    Comm* c = nccl_id ? (Comm*)new NcclComm(world, shard, nccl_id) : (Comm*)new LocalComm(1);
     g = new ShardGroup<float>();
     g->dtype = dtype;
     g->init(m, n, rank, starts, nnz, (const float*)X_rows, mask_rows, c, device);

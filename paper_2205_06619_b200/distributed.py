@@ -81,13 +81,14 @@ def exchange_nccl_id(dist=None) -> bytes | None:
 
 
 def fast_stmf_sharded(R: MaskedMatrix, rank: int, config: RunConfig, device: int | None = None,
-                      session_factory=None):
+                      session_factory=None, init=None):
     """fast_stmf with the work rows sharded over the ranks of the default process
     group (binary32).  Returns (FactorPair, Trajectory) on every rank.
 
     ``session_factory(plan, work, rank, nccl_id)`` may replace the device session
     (host-logic tests on CPU); it must return an object with set_factors / run /
-    get_factors like ``_ext.Session``.
+    get_factors like ``_ext.Session``.  ``init``: optional warm-start (U, V) in the
+    original orientation (engine.run_fit).
     """
     dist = _dist()
     world, me = dist.get_world_size(), dist.get_rank()
@@ -99,7 +100,11 @@ def fast_stmf_sharded(R: MaskedMatrix, rank: int, config: RunConfig, device: int
     wall = config.budget_seconds is not None
     t0 = time.perf_counter()
     work, orientation = _orient_faststmf(R, rng)
-    U0 = acol_means(work, rank, config.acol_columns, rng)
+    V0 = None
+    if init is None:
+        U0 = acol_means(work, rank, config.acol_columns, rng)
+    else:
+        U0, V0 = orientation.apply_factors(np.asarray(init[0], np.float32), np.asarray(init[1], np.float32))
     plan = ShardPlan(work, world, me)
     nccl_id = exchange_nccl_id(dist)
     if session_factory is None:
@@ -107,7 +112,7 @@ def fast_stmf_sharded(R: MaskedMatrix, rank: int, config: RunConfig, device: int
                                  plan.row_nnz, world, me, nccl_id, device)
     else:
         s = session_factory(plan, work, rank, nccl_id)
-    s.set_factors(plan.rows(U0))
+    s.set_factors(plan.rows(U0), V0)
     t_init = time.perf_counter() - t0 if wall else 0.0
     budget_seconds = max(config.budget_seconds - t_init, 1e-9) if wall else None
     tt, te, counts = s.run(config.budget_sweeps, budget_seconds, config.epsilon)

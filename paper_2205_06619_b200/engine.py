@@ -163,13 +163,18 @@ def _run_bymatrix(s: "FitSession", config: RunConfig, rng: np.random.Generator, 
     return np.array(tt), np.array(te), counts
 
 
-def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int | None = None):
+def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int | None = None,
+            init=None):
     """Budgeted outer loop (engine.py:313-348) with the sweeps on the device.
 
     ``strategy`` is a ``StrategySpec`` (or an object with ``.spec``) or ``BASELINE``
     ("STMF", the classic element-wise method, engine.py:351-385).  The FastSTMF
     strategy runs its sweeps as device-resident CUDA graphs; the other methods run
     the same device kernels under a host-driven batch loop.
+
+    ``init`` (an extension; the reference always starts from Random-Acol): a warm
+    start (U, V) or FactorPair in the original orientation, used instead of the Acol
+    draws (the RNG stream then continues right after the orientation draws).
     """
     spec = getattr(strategy, "spec", strategy)
     family, selection = _strategy_codes(spec)
@@ -182,9 +187,16 @@ def run_fit(R: MaskedMatrix, rank: int, strategy, config: RunConfig, device: int
     wall_clock = config.budget_seconds is not None
     t0 = time.perf_counter()
     work, orientation = _orient(spec, R, rng)
-    U0 = acol_means(work, rank, config.acol_columns, rng)
+    V0 = None
+    if init is None:
+        U0 = acol_means(work, rank, config.acol_columns, rng)
+    else:
+        Ui, Vi = (init.U, init.V) if isinstance(init, FactorPair) else init
+        if np.shape(Ui) != (R.m, rank) or np.shape(Vi) != (rank, R.n):
+            raise ValueError(f"init shapes {np.shape(Ui)}, {np.shape(Vi)} do not match {(R.m, rank)}, {(rank, R.n)}")
+        U0, V0 = orientation.apply_factors(np.asarray(Ui, dtype=R.dtype), np.asarray(Vi, dtype=R.dtype))
     with FitSession(work, rank, device) as s:
-        s.set_factors(U0)
+        s.set_factors(U0, V0)
         if (family, selection) != (_ext.FAMILY_BYROW, _ext.SEL_TD_A):
             s.set_strategy(family, selection)
         if config.audit:

@@ -76,13 +76,14 @@ def parse_method(name: str):
     raise ValueError(f"cannot parse method name {name!r}")
 
 
-def fit(R: MaskedMatrix, rank: int, method, config: RunConfig, device: int | None = None):
-    """Fit R with a method name or StrategySpec (strategies.py:351-357)."""
+def fit(R: MaskedMatrix, rank: int, method, config: RunConfig, device: int | None = None, init=None):
+    """Fit R with a method name or StrategySpec (strategies.py:351-357).  ``init``:
+    optional warm-start factors (engine.run_fit)."""
     if isinstance(method, str):
         method = parse_method(method)
-    return run_fit(R, rank, method, config, device=device)
+    return run_fit(R, rank, method, config, device=device, init=init)
 
 
-def fast_stmf(R: MaskedMatrix, rank: int, config: RunConfig, device: int | None = None):
+def fast_stmf(R: MaskedMatrix, rank: int, config: RunConfig, device: int | None = None, init=None):
     """FastSTMF = ByRow, RandPermR, TD_A, wide (strategies.py:360-362), on the B200."""
-    return fit(R, rank, FASTSTMF, config, device=device)
+    return fit(R, rank, FASTSTMF, config, device=device, init=init)

@@ -157,6 +157,18 @@ class Orientation:
             work = work.permute_cols(self.col_perm)
         return work
 
+    def apply_factors(self, U: np.ndarray, V: np.ndarray):
+        """Factors of the original orientation -> the work orientation (inverse of
+        ``restore``): a warm start's (U, V) for the work matrix ``apply(R)``."""
+        U, V = np.asarray(U), np.asarray(V)
+        if self.transposed:
+            U, V = V.T, U.T
+        if self.row_perm is not None:
+            U = U[self.row_perm.forward, :]
+        if self.col_perm is not None:
+            V = V[:, self.col_perm.forward]
+        return np.ascontiguousarray(U), np.ascontiguousarray(V)
+
     def restore(self, U: np.ndarray, V: np.ndarray):
         if self.row_perm is not None:
             U = U[self.row_perm.inverse, :]

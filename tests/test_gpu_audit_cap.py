@@ -61,3 +61,16 @@ def test_attempt_cap_rejects_seq_selection():
         s.set_max_attempts(5)
         with pytest.raises(_ext.StmfError, match="attempt cap"):
             s.run(budget_sweeps=1, epsilon=0.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_warm_start_continues_the_fit(dtype):
+    """fast_stmf(init=...) from the factors after sweep 1 reaches the 2-sweep fit's
+    factors bit for bit (ByRow sweeps draw no random numbers)."""
+    R = _crop(gen.config2(), 150, 90, dtype)  # tall: exercises the transposed orientation
+    p1, _ = pkg.fast_stmf(R, 5, pkg.RunConfig(rank=5, budget_sweeps=1, epsilon=0.0, seed=3))
+    p2, t2 = pkg.fast_stmf(R, 5, pkg.RunConfig(rank=5, budget_sweeps=2, epsilon=0.0, seed=3))
+    pw, tw = pkg.fast_stmf(R, 5, pkg.RunConfig(rank=5, budget_sweeps=1, epsilon=0.0, seed=3), init=(p1.U, p1.V))
+    assert np.array_equal(pw.U, p2.U) and np.array_equal(pw.V, p2.V)
+    assert tw.errors[0] == t2.errors[len(t2.errors) - len(tw.errors)]
+    assert tw.errors[-1] == t2.errors[-1]

@@ -82,6 +82,35 @@ def test_sharded_world1_is_the_nccl_entry_point():
     assert np.array_equal(te, te1)
 
 
+def _nccl_id():
+    import ctypes
+    buf = np.zeros(256, np.uint8)
+    size = np.array([256], np.int64)
+    _ext._check(_ext.lib().stmf_nccl_unique_id(_ext._p(buf), size.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    return bytes(buf[: int(size[0])])
+
+
+@pytest.mark.parametrize("seed,m,n,r,frac,sweeps", [(41, 60, 90, 4, 0.5, 3), (42, 128, 200, 10, 0.7, 2)])
+def test_sharded_world1_over_a_real_nccl_communicator(seed, m, n, r, frac, sweeps):
+    """stmf_create_sharded with an NCCL id at world size 1: ncclCommInitRank(nranks=1)
+    and every collective of the sharded engine (MIN on binary32, SUM on int64 limbs,
+    all-gather, broadcast) execute through libnccl, and the fit equals the
+    single-device engine bit for bit."""
+    work, U0 = _case(seed, m, n, r, frac)
+    te1, U1, V1, c1, _ = _single(work, U0, r, sweeps)
+    nnz = work.mask.sum(axis=1)
+    s = _ext.Session.sharded(work.values, work.mask, r, work.m, np.array([0, work.m]), nnz, 1, 0, _nccl_id())
+    try:
+        s.set_factors(U0)
+        tt, te, c = s.run(budget_sweeps=sweeps, epsilon=0.0)
+        U, V = s.get_factors()
+    finally:
+        s.close()
+    assert np.array_equal(te, te1)
+    assert np.array_equal(U, U1) and np.array_equal(V, V1)
+    assert c["attempts"] == c1["attempts"]
+
+
 def test_sharded_rejects_fp64():
     X = np.ones((4, 5))
     M = np.ones((4, 5), bool)

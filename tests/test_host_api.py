@@ -137,3 +137,19 @@ def test_config4_generator_small_is_covered_and_blocked():
     assert 0.8 < rates.mean() < 0.95  # Beta(9, 1) mean 0.9
     R2 = gen.config4(seed=3, m=256, n=300, rank=4, blocks=4)
     assert np.array_equal(R.mask, R2.mask) and np.array_equal(R.values[R.mask], R2.values[R2.mask])
+
+
+def test_orientation_apply_factors_inverts_restore():
+    import numpy as np
+    from paper_2205_06619_b200.tropical import Permutation
+    from paper_2205_06619_b200.types import Orientation
+    rng = np.random.default_rng(0)
+    U, V = rng.random((7, 3)), rng.random((3, 5))
+    for tr in (False, True):
+        rows = 5 if tr else 7
+        cols = 7 if tr else 5
+        o = Orientation(tr, Permutation.random(rows, rng), Permutation.random(cols, rng))
+        Uw, Vw = o.apply_factors(U, V)
+        assert Uw.shape == (rows, 3) and Vw.shape == (3, cols)
+        U2, V2 = o.restore(Uw, Vw)
+        assert np.array_equal(U2, U) and np.array_equal(V2, V)

@@ -36,7 +36,7 @@ class OracleShard:
     def __init__(self, plan, work, rank):
         self.plan, self.work, self.rank = plan, work, rank
 
-    def set_factors(self, U_rows):
+    def set_factors(self, U_rows, V=None):
         # the full U0 is rebuilt from every rank's rows by the caller's all-gather
         # at the end; here each rank needs it whole: gather it now
         parts = [None] * dist.get_world_size()
