@@ -123,6 +123,8 @@ def lib():
         "stmf_create_sim_group": [ctypes.POINTER(_vp), _int, _i64, _i64, _int, _vp, _vp, _int, _int],
         "stmf_bench_maxplus": [_i64, _i64, _int, _dbl, ctypes.c_uint64, _int, _int, _int, _vp, _vp, _vp, _vp,
                                _vp],
+        "stmf_bench_maxplus_layout": [_i64, _i64, _int, _dbl, ctypes.c_uint64, _int, _int, _int, _int, _vp, _vp,
+                                      _vp, _vp, _vp],
         "stmf_set_strategy": [_vp, _int, _int],
         "stmf_row_scores": [_vp, _vp],
         "stmf_matrix_candidates": [_vp, _vp, _vp, _vp, _vp],
@@ -151,7 +153,7 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_product_given", "stmf_col_scores", "stmf_residuate", "stmf_try_update",
                     "stmf_attempt", "stmf_bench_product", "stmf_trop_matmul",
                     "stmf_stream", "stmf_set_profiling", "stmf_counters", "stmf_nccl_unique_id",
-                    "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus",
+                    "stmf_create_sharded", "stmf_create_sim_group", "stmf_bench_maxplus", "stmf_bench_maxplus_layout",
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
                     "stmf_csv_close", "stmf_release_memory",
@@ -164,18 +166,23 @@ SEL_TD_A, SEL_TD, SEL_TD_B, SEL_SEQ = 0, 1, 2, 3
 
 
 def bench_maxplus(m: int, n: int, rank: int, density: float, seed: int = 0, reps: int = 5,
-                  flush_l2: bool = True, device: int | None = None, want_data: bool = False):
-    """Config-5 masked max-plus product + error microbench on device-generated data."""
-    out = np.zeros(6, np.float64)
+                  flush_l2: bool = True, device: int | None = None, want_data: bool = False, layout: str = "dense"):
+    """Config-5 masked max-plus product + error microbench on device-generated data.
+    layout: "dense" (k_maxplus_err), "sampled" (given values only, k_maxplus_err_sampled)
+    or "auto" (sampled at density <= 0.35)."""
+    code = {"dense": 0, "sampled": 1, "auto": -1}[layout]
+    out = np.zeros(8, np.float64)
     X = np.empty((m, n), np.float32) if want_data else None
     M = np.empty(m * n // 32, np.uint32) if want_data else None
     U = np.empty((rank, m), np.float32) if want_data else None
     V = np.empty((rank, n), np.float32) if want_data else None
     p = lambda a: None if a is None else _p(a)  # noqa: E731
-    _check(lib().stmf_bench_maxplus(m, n, rank, float(density), int(seed), int(reps), int(flush_l2),
-                                    default_device() if device is None else int(device), _p(out),
-                                    p(X), p(M), p(U), p(V)))
-    res = dict(zip(("avg_ms", "best_ms", "objective", "given", "gbs", "gpairs_per_s"), out.tolist()))
+    _check(lib().stmf_bench_maxplus_layout(m, n, rank, float(density), int(seed), int(reps), int(flush_l2),
+                                           default_device() if device is None else int(device), code, _p(out),
+                                           p(X), p(M), p(U), p(V)))
+    res = dict(zip(("avg_ms", "best_ms", "objective", "given", "gbs", "gpairs_per_s", "layout", "bytes"),
+                   out.tolist()))
+    res["layout"] = "sampled" if res["layout"] == 1 else "dense"
     if want_data:
         mask = np.unpackbits(M.view(np.uint8), bitorder="little").reshape(m, n).astype(bool)
         res["data"] = (X, mask, U.T.copy(), V)

@@ -14,6 +14,7 @@
 //      reference order with f < err wins (FitRun._attempt, engine.py:283);
 //   4. commit: column k of U, row k of V.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -717,6 +718,11 @@ struct Session : SessionBase {
     }
     ssync();
     sync_factor_copies(-1);
+    // new factors start a new speculation history (the depths of another state say
+    // nothing about this one): first visits use the initial batch schedule
+    if ((int64_t)row_depth.size() == m) std::fill(row_depth.begin(), row_depth.end(), 0);
+    rdepth_on_dev = false;
+    depth_ema = 0;
     have_factors = true;
     cur_valid = false;
     dirty = true;
@@ -2329,11 +2335,24 @@ __global__ void k_popcount(int64_t words, const uint32_t* __restrict__ mask, u64
 
 // config-5 microbench: data generated on the device (seeded counter-based RNG:
 // X, U, V ~ U[-1, 1) on the 2^-23 grid, iid mask with P(given) = density)
+// layout: 0 = dense tiles (k_maxplus_err), 1 = sampled / compacted (k_maxplus_err_sampled),
+// -1 = automatic (sampled when density <= 0.35 and r <= 64: fewer bytes and only given
+// entries computed; measured crossover, profiles/r02_c5_sampled.md)
+template <int RQ>
+static void launch_sampled(unsigned grid, cudaStream_t st, int64_t m, int64_t n, const uint32_t* M, const float* vals,
+                           const int64_t* off, const float* Urm, const float* Vrm, u64* acc, int* flags, int F,
+                           double lim) {
+  k_maxplus_err_sampled<RQ><<<grid, 256, sp_smem_bytes<RQ>(), st>>>(m, n, M, vals, off, Urm, Vrm, acc, flags, F, lim);
+}
+
 static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint64_t seed, int reps, int flush,
                                int device, double* out, float* X_out, uint32_t* mask_out, float* U_out,
-                               float* V_out) {
+                               float* V_out, int layout = 0) {
   if (m % kMpTR || n % kMpTC) fail(STMF_ERR_INVALID, "m must be a multiple of %d and n of %d", kMpTR, kMpTC);
   if (r < 1) fail(STMF_ERR_INVALID, "rank must be >= 1");
+  if (layout < 0) layout = (density <= 0.35 && r <= 64 && m % kSpT == 0 && n % kSpT == 0) ? 1 : 0;
+  if (layout == 1 && (m % kSpT || n % kSpT)) fail(STMF_ERR_INVALID, "sampled layout: m and n must be multiples of %d", kSpT);
+  if (layout == 1 && r > 64) fail(STMF_ERR_INVALID, "sampled layout: rank must be <= 64");
   CK(cudaSetDevice(device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
@@ -2413,6 +2432,42 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaFuncSetAttribute(k_maxplus_err<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxplusDynSmem));
   }
   auto kernt = kc_sel == 4 ? k_maxplus_err<4, true> : kc_sel == 8 ? k_maxplus_err<8, true> : k_maxplus_err<16, true>;
+  // sampled layout: packed given values per tile + padded row-major factors
+  DevBuf<float> vals, Urm, Vrm;
+  DevBuf<int64_t> tcnt, toff;
+  int rq = 1;
+  while (4 * rq < r) rq *= 2;
+  unsigned sgrid = 0;
+  u64 given_h = 0;
+  if (layout == 1) {
+    int RS = sp_stride(rq);
+    int64_t T = (m / kSpT) * (n / kSpT);
+    tcnt.alloc(T + 1); toff.alloc(T + 1);
+    CK(cudaMemsetAsync(tcnt.p + T, 0, sizeof(int64_t), st));
+    k_sp_tile_count<<<gb, 256, 0, st>>>(m, n, M.p, tcnt.p); LAUNCH_CK();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt.p, toff.p, T + 1, st));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, tcnt.p, toff.p, T + 1, st));
+    CK(cudaMemcpyAsync(&given_h, toff.p + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    vals.alloc(std::max<u64>(given_h, 1));
+    k_sp_tile_fill<<<gb, 256, 0, st>>>(m, n, M.p, X.p, toff.p, vals.p); LAUNCH_CK();
+    Urm.alloc((size_t)m * RS); Vrm.alloc((size_t)n * RS);
+    k_sp_factor<<<nblk(m * RS, 256), 256, 0, st>>>(m, r, RS, Ut.p, Urm.p); LAUNCH_CK();
+    k_sp_factor<<<nblk(n * RS, 256), 256, 0, st>>>(n, r, RS, V.p, Vrm.p); LAUNCH_CK();
+    const void* kf = rq == 1 ? (const void*)k_maxplus_err_sampled<1> : rq == 2 ? (const void*)k_maxplus_err_sampled<2>
+                   : rq == 4 ? (const void*)k_maxplus_err_sampled<4> : rq == 8 ? (const void*)k_maxplus_err_sampled<8>
+                   : (const void*)k_maxplus_err_sampled<16>;
+    size_t smem = rq == 1 ? sp_smem_bytes<1>() : rq == 2 ? sp_smem_bytes<2>() : rq == 4 ? sp_smem_bytes<4>()
+                : rq == 8 ? sp_smem_bytes<8>() : sp_smem_bytes<16>();
+    CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, smem));
+    sgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)prop.multiProcessorCount * std::max(per_sm, 1)));
+    CK(cudaStreamSynchronize(st));
+  }
   double total = 0, best = 1e30;
   u64 h[2] = {0, 0};
   for (int rep = 0; rep < std::max(reps, 1); rep++) {
@@ -2420,7 +2475,11 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
-    if (tma)
+    if (layout == 1) {
+      auto L = rq == 1 ? launch_sampled<1> : rq == 2 ? launch_sampled<2> : rq == 4 ? launch_sampled<4>
+             : rq == 8 ? launch_sampled<8> : launch_sampled<16>;
+      L(sgrid, st, m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F, exact_limit);
+    } else if (tma)
       kernt<<<grid, 256, kMaxplusDynSmem, st>>>(m, n, r, X.p, M.p, Ut.p, V.p, acc.p, flags.p, F, exact_limit, xmap,
                                                 umap, vmap);
     else
@@ -2449,13 +2508,17 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   cudaStreamDestroy(st);
   if (hf & 6) fail(STMF_ERR_NUMERIC, "exact objective window violated (flags %d)", hf);
   double avg = total / std::max(reps, 1);
-  double bytes = (double)m * n * 4.0 + (double)words * 4.0 + (double)r * (m + n) * 4.0;
+  // algorithmic bytes: dense tiles read every value; the sampled layout only the given ones
+  double bytes = (layout == 1 ? (double)given * 4.0 : (double)m * n * 4.0) + (double)words * 4.0 +
+                 (double)r * (m + n) * 4.0;
   out[0] = avg;
   out[1] = best;
   out[2] = fx_to_double(h[1], h[0], F);
   out[3] = (double)given;
   out[4] = bytes / (avg * 1e-3) / 1e9;                    // algorithmic GB/s
-  out[5] = (double)m * n * r / (avg * 1e-3) / 1e9;        // G (entry, k) pairs / s (dense)
+  out[5] = (double)(layout == 1 ? given : m * n) * r / (avg * 1e-3) / 1e9;  // G computed (entry, k) pairs / s
+  out[6] = layout;
+  out[7] = bytes;
 }
 
 struct stmf_session {
@@ -2730,7 +2793,20 @@ int stmf_create(stmf_session** out, int dtype, int64_t m, int64_t n, int rank, c
 int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps, int flush_l2,
                        int device, double* out6, float* X_out, uint32_t* mask_out, float* U_out, float* V_out) {
   if (!out6) return set_err(STMF_ERR_INVALID, "null output");
-  GUARD(maxplus_bench_impl(m, n, rank, density, seed, reps, flush_l2, device, out6, X_out, mask_out, U_out, V_out));
+  double o[8];
+  GUARD({
+    maxplus_bench_impl(m, n, rank, density, seed, reps, flush_l2, device, o, X_out, mask_out, U_out, V_out, 0);
+    memcpy(out6, o, sizeof(double) * 6);
+  });
+}
+
+int stmf_bench_maxplus_layout(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps, int flush_l2,
+                              int device, int layout, double* out8, float* X_out, uint32_t* mask_out, float* U_out,
+                              float* V_out) {
+  if (!out8) return set_err(STMF_ERR_INVALID, "null output");
+  if (layout < -1 || layout > 1) return set_err(STMF_ERR_INVALID, "layout must be -1, 0 or 1");
+  GUARD(maxplus_bench_impl(m, n, rank, density, seed, reps, flush_l2, device, out8, X_out, mask_out, U_out, V_out,
+                           layout));
 }
 
 int stmf_nccl_unique_id(void* out, int64_t* bytes) {

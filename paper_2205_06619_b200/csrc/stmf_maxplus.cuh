@@ -219,6 +219,177 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
   }
 }
 
+// ----------------------------------------------------------------------------
+// Sampled (compacted) variant for low densities: only the given entries are read and
+// computed.  The reference's objective ranges over the given entries only
+// (tropical.py:214-222: b_norm of the residual at mask), so a layout that stores just
+// the given values (plus the bit-packed mask that says where they are) is the
+// algorithmic minimum: m*n/8 + 4*given bytes, versus m*n*(4 + 1/8) for the dense tile.
+//
+// Layout: tiles of 128 x 128 entries in row-major tile order; a tile's given values
+// are packed contiguously, row-major within the tile (tile_off[t] = first value of
+// tile t, an exclusive scan of the tile counts).  Factors row-major with a padded
+// stride RS (U: m x RS, V: n x RS; padding = -inf, so it never wins a max).
+//
+// Per tile (one block of 256 threads, persistent over tiles): the factor rows of the
+// tile are staged in shared memory; then per chunk of 32 rows the mask words are
+// decoded into a list of (row, column) codes in exactly the packed-value order (block
+// scan of the row counts, popc ranks within words), and the threads walk that list:
+// one coalesced value load + RQ float4 loads of each factor row per given entry,
+// FADD2 pairs and 3-input max.  Exact accumulation as the dense kernel.
+constexpr int kSpT = 128;      // tile edge
+constexpr int kSpRows = 32;    // rows decoded per chunk (list <= 32 * 128 codes)
+__host__ __device__ constexpr int sp_stride(int rq) { return rq % 2 ? 4 * rq : 4 * rq + 4; }
+
+template <int RQ>
+__global__ void __launch_bounds__(256)
+k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, const float* __restrict__ vals,
+                      const int64_t* __restrict__ tile_off, const float* __restrict__ Urm,
+                      const float* __restrict__ Vrm, u64* __restrict__ acc, int* __restrict__ flags, int F,
+                      double exact_limit) {
+  constexpr int RS = sp_stride(RQ);
+  extern __shared__ __align__(16) unsigned char sp_smem[];
+  float* Us = reinterpret_cast<float*>(sp_smem);
+  float* Vs = Us + kSpT * RS;
+  uint16_t* list = reinterpret_cast<uint16_t*>(Vs + kSpT * RS);
+  __shared__ int rowcnt[kSpRows], rowoff[kSpRows + 1];
+  __shared__ double red[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t ntx = n / kSpT, T = (m / kSpT) * ntx;
+  const int64_t wpr = n / 32;  // mask words per matrix row
+  double part = 0.0;
+  for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const int64_t row0 = (t / ntx) * kSpT, col0 = (t % ntx) * kSpT;
+    // factor rows of the tile (L2-resident across tiles)
+    for (int e = tid; e < kSpT * RQ; e += 256) {
+      int rr = e / RQ, q = e - rr * RQ;
+      *reinterpret_cast<float4*>(Us + rr * RS + 4 * q) =
+          __ldg(reinterpret_cast<const float4*>(Urm + (row0 + rr) * RS) + q);
+      *reinterpret_cast<float4*>(Vs + rr * RS + 4 * q) =
+          __ldg(reinterpret_cast<const float4*>(Vrm + (col0 + rr) * RS) + q);
+    }
+    int64_t vbase = tile_off[t];
+    for (int c0 = 0; c0 < kSpT; c0 += kSpRows) {
+      // row counts of the chunk: warp w, rows 4w..4w+3; lanes 0..3 hold the 4 words
+      const uint32_t* mrow = mask + (row0 + c0) * wpr + col0 / 32;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        int rl = wid * 4 + q;
+        uint32_t w = lane < 4 ? __ldg(mrow + rl * wpr + lane) : 0u;
+        int c = __popc(w);
+        c += __shfl_xor_sync(0xffffffffu, c, 1);
+        c += __shfl_xor_sync(0xffffffffu, c, 2);
+        if (lane == 0) rowcnt[rl] = c;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        int v = rowcnt[lane], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        rowoff[lane] = x - v;
+        if (lane == 31) rowoff[kSpRows] = x;
+      }
+      __syncthreads();
+      // decode: lane = column within a word; codes in packed (row-major) order
+      const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        int rl = wid * 4 + q;
+        int pos = rowoff[rl];
+#pragma unroll
+        for (int wi = 0; wi < 4; wi++) {
+          uint32_t w = __ldg(mrow + rl * wpr + wi);
+          if ((w >> lane) & 1u) list[pos + __popc(w & lt)] = (uint16_t)(((c0 + rl) << 7) | (wi * 32 + lane));
+          pos += __popc(w);
+        }
+      }
+      __syncthreads();
+      const int total = rowoff[kSpRows];
+      const float* vc = vals + vbase;
+      for (int e = tid; e < total; e += 256) {
+        float x = __ldg(vc + e);
+        int code = list[e];
+        const float4* ur = reinterpret_cast<const float4*>(Us + (code >> 7) * RS);
+        const float4* vr = reinterpret_cast<const float4*>(Vs + (code & 127) * RS);
+        float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
+#pragma unroll
+        for (int q = 0; q < RQ; q++) {
+          float4 u = ur[q], v = vr[q];
+          float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
+          float2 b = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
+          p0 = max3f(p0, a.x, a.y);
+          p1 = max3f(p1, b.x, b.y);
+        }
+        part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
+      }
+      vbase += total;
+      __syncthreads();
+    }
+  }
+  for (int o = 16; o; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+  if (lane == 0) red[wid] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; w++) s = __dadd_rn(s, red[w]);
+    int fl = 0;
+    if (!(s < exact_limit)) fl |= 4;
+    u64 hi, lo;
+    fx_from_double(s, F, hi, lo, fl);
+    fx_atomic_add(acc, hi, lo);
+    if (fl) atomicOr(flags, fl);
+  }
+}
+
+template <int RQ>
+constexpr size_t sp_smem_bytes() {
+  return sizeof(float) * 2 * kSpT * sp_stride(RQ) + sizeof(uint16_t) * kSpRows * kSpT;
+}
+
+// data preparation for the sampled layout (not timed): per-tile given counts, then the
+// packed values in the kernel's order, and the padded row-major factor copies
+__global__ void k_sp_tile_count(int64_t m, int64_t n, const uint32_t* __restrict__ mask, int64_t* __restrict__ cnt) {
+  const int64_t ntx = n / kSpT, T = (m / kSpT) * ntx, wpr = n / 32;
+  int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t* mt = mask + (t / ntx) * kSpT * wpr + (t % ntx) * (kSpT / 32);
+    int c = 0;
+    for (int e = lane; e < kSpT * 4; e += 32) c += __popc(mt[(e >> 2) * wpr + (e & 3)]);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[t] = c;
+  }
+}
+
+__global__ void k_sp_tile_fill(int64_t m, int64_t n, const uint32_t* __restrict__ mask, const float* __restrict__ X,
+                               const int64_t* __restrict__ tile_off, float* __restrict__ vals) {
+  const int64_t ntx = n / kSpT, T = (m / kSpT) * ntx, wpr = n / 32;
+  int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row0 = (t / ntx) * kSpT, col0 = (t % ntx) * kSpT;
+    int64_t pos = tile_off[t];
+    for (int rl = 0; rl < kSpT; rl++)
+      for (int wi = 0; wi < 4; wi++) {
+        uint32_t w = mask[(row0 + rl) * wpr + col0 / 32 + wi];
+        if ((w >> lane) & 1u) vals[pos + __popc(w & ((1u << lane) - 1u))] = X[(row0 + rl) * n + col0 + wi * 32 + lane];
+        pos += __popc(w);
+      }
+  }
+}
+
+// factor k-major (r x len) -> row-major padded (len x RS), padding -inf
+__global__ void k_sp_factor(int64_t len, int r, int RS, const float* __restrict__ src, float* __restrict__ dst) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= len * RS) return;
+  int64_t i = t / RS;
+  int k = (int)(t - i * RS);
+  dst[t] = k < r ? src[(int64_t)k * len + i] : -CUDART_INF_F;
+}
+
 // counter-based uniform floats on the 2^-24 grid in [lo, lo + 2): splitmix64
 __device__ __forceinline__ u64 splitmix64(u64 x) {
   x += 0x9E3779B97F4A7C15ull;

@@ -1,5 +1,9 @@
-"""Config-5 kernel (tiled masked max-plus product + exact error reduction) against
-the CPU restatement on device-generated data; plus the dense prediction product."""
+"""Config-5 kernels (masked max-plus product + exact error reduction, BASELINE.json
+configs[4]) against the CPU restatement on device-generated data: the dense-tile
+kernel and the sampled (given-values-only) kernel, at toy shapes and at the config's
+real 4096^2 (every rank x density) and 16384^2 (rank 4) points.  Both layouts compute
+the exact sum of the binary32 residuals (tropical.py:214-222 restated in fp32), so
+they agree with each other and with the restatement bit for bit."""
 
 import math
 
@@ -25,6 +29,39 @@ def test_maxplus_err_matches_restatement(m, n, r, d):
     assert res["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
 
 
+@pytest.mark.parametrize("m,n,r,d", [(128, 128, 4, 0.1), (256, 384, 13, 0.3), (384, 128, 64, 0.05),
+                                     (128, 256, 1, 1.0), (256, 256, 33, 0.0)])
+def test_sampled_layout_matches_dense_and_restatement(m, n, r, d):
+    a = _ext.bench_maxplus(m, n, r, d, seed=7 * m + r, reps=1, flush_l2=False, layout="dense")
+    b = _ext.bench_maxplus(m, n, r, d, seed=7 * m + r, reps=2, flush_l2=False, layout="sampled", want_data=True)
+    assert b["layout"] == "sampled" and b["given"] == a["given"]
+    assert b["objective"] == a["objective"]
+    X, M, U, V = b["data"]
+    assert b["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
+
+
+@pytest.mark.parametrize("r", [4, 16, 64])
+@pytest.mark.parametrize("d", [0.1, 0.5, 1.0])
+def test_config5_4096_matches_restatement(r, d):
+    """BASELINE.json configs[4] at m = n = 4096: every (rank, density) point; the
+    automatic layout choice, plus the other layout, against the restatement."""
+    res = _ext.bench_maxplus(4096, 4096, r, d, seed=5, reps=1, flush_l2=False, want_data=True, layout="auto")
+    X, M, U, V = res["data"]
+    ref = oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
+    assert res["objective"] == ref
+    other = "dense" if res["layout"] == "sampled" else "sampled"
+    assert _ext.bench_maxplus(4096, 4096, r, d, seed=5, reps=1, flush_l2=False, layout=other)["objective"] == ref
+
+
+def test_config5_16384_rank4_matches_restatement():
+    res = _ext.bench_maxplus(16384, 16384, 4, 0.1, seed=9, reps=1, flush_l2=False, want_data=True, layout="auto")
+    X, M, U, V = res["data"]
+    assert res["layout"] == "sampled"
+    assert res["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
+
+
 def test_maxplus_rejects_unaligned():
     with pytest.raises(_ext.StmfError, match="multiple"):
         _ext.bench_maxplus(100, 128, 4, 0.5)
+    with pytest.raises(_ext.StmfError, match="multiples of 128"):
+        _ext.bench_maxplus(64, 128, 4, 0.1, layout="sampled")
