@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample (1 process)")
     ap.add_argument("--ref-seconds", type=float, default=None,
-                    help="reference-arm sample per process (default: 6 s per step, 45..150 s)")
+                    help="reference-arm sample per process (default: 6 s per step, 90..150 s)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -240,7 +240,7 @@ def run_reference(args):
     from paper_2205_06619_b200 import gen
     C = gen.CONFIGS[args.config]
     procs = os.cpu_count() or 1
-    seconds = args.ref_seconds or float(min(150.0, max(45.0, 6.0 * args.steps)))
+    seconds = args.ref_seconds or float(min(150.0, max(90.0, 6.0 * args.steps)))
     if args.warmup > 0:  # untimed: page in numpy, the data and one row visit
         reference_sample(args.config, 2.0, 1)
     r = reference_sample(args.config, seconds, procs)
@@ -298,7 +298,9 @@ def run_b200(args):
         s = _ext.Session.sharded(plan.rows(work.values), plan.rows(work.mask), r, m, plan.starts, plan.row_nnz,
                                  world, rank, exchange_nccl_id(dist), local)
         rows = plan.rows
+        comm = s.comm_info()
     else:
+        comm = None
         s = _ext.Session(work.values, work.mask, r, device=local)
         rows = lambda a: a  # noqa: E731
     stream = torch.cuda.ExternalStream(s.stream_handle(), device=torch.device("cuda", local))
@@ -369,6 +371,7 @@ def run_b200(args):
             "attempts_per_step": attempts[0], "accepts_per_step": accepts[0], "evaluated_per_step": evaluated[0],
             "error_after_step": ends[0], "state_check": state_check, "deterministic_steps": deterministic,
             "gpu_launches": int(c1["launches"] - c0["launches"]),
+            "comm": comm, "comm_nranks_ok": None if comm is None else (comm["nranks"] == world and comm["kind"] == "nccl"),
             "library_sorts": int(c1["cub_sorts"] - c0["cub_sorts"]),
             "roofline": roof,
             "clocks": clk.summary(),
@@ -442,7 +445,15 @@ def roofline(args, work, prof, step_s, clk):
     achieved = 2 * b_pass / avg_s / 1e9
     prof = phaseB_profile(args.config) or {}
     rate = evaluated * N / (b_ns / 1e9)  # (entry, evaluation) pairs per second in phase B
-    issue = None
+    issue = l1 = None
+    if "duration_us" in prof:
+        # the binding resource: L1 data-pipe wavefronts (the gathers), scaled from the
+        # capture's utilisation by the live (entry, evaluation) rate
+        cap_rate = prof["evals"] * prof["given"] / (prof["duration_us"] * 1e-6)
+        l1 = {"capture_frac": prof.get("l1_wavefront_frac"), "capture_pairs_per_s": cap_rate,
+              "live_pairs_per_s": rate,
+              "frac": prof.get("l1_wavefront_frac", 0) * rate / cap_rate if prof.get("l1_wavefront_frac") else None,
+              "sectors_per_pair": prof.get("l1_global_ld_sectors", 0) / (prof["evals"] * prof["given"])}
     if "warp_instructions" in prof:
         ipe = prof["warp_instructions"] / (prof["evals"] * prof["given"])
         prop = torch.cuda.get_device_properties(0)
@@ -460,9 +471,11 @@ def roofline(args, work, prof, step_s, clk):
             "algorithmic_bytes_per_launch": 2 * b_pass, "evals_per_launch": evaluated / nb,
             "avg_launch_us": avg_s * 1e6, "launches": nb, "share_of_step": (b_ns / 1e9) / step_s,
             "timing": "CUDA events around every phase-B launch of one extra (untimed) step",
-            "peak_source": peak_src, "issue": issue, "binding": "issue" if issue else None,
+            "peak_source": peak_src, "issue": issue, "l1": l1, "binding": "l1_wavefronts" if l1 else None,
             "note": "HBM is not phase B's bound: one launch serves a whole batch of evaluations from one "
-                    "streaming of the entry data; the binding resource is instruction issue (roofline.issue)"}
+                    "streaming of the entry data (traffic = that streaming incl. the product caches); the "
+                    "binding resource is the L1 data pipe (the first-residuation gathers, roofline.l1), "
+                    "instruction issue second (roofline.issue); profiles/r02_phaseB_c3.md"}
 
 
 def c5_microbench(_ext, local):

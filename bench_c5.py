@@ -5,7 +5,12 @@ per case with algorithmic GB/s (X + bit mask + factors per launch) against the
 measured HBM copy peak and dense (entry, k) pairs/s against the FP32 ALU issue
 bound (one FADD2 + one 3-input FMNMX per two (entry, k) pairs per lane).
 
+Layouts: "dense" (k_maxplus_err: every entry's value read and computed) and "sampled"
+(k_maxplus_err_sampled: only the given values, packed per tile, plus the bit mask;
+only given entries computed).  GB/s counts each layout's own algorithmic bytes.
+
   python bench_c5.py [--sizes 4096,16384,65536] [--ranks 4,16,64] [--density 0.1,0.5,1.0] [--reps 5]
+                     [--layouts dense,sampled]
 """
 
 import argparse
@@ -23,6 +28,7 @@ def main():
     ap.add_argument("--ranks", default="4,16,64")
     ap.add_argument("--density", default="0.1,0.5,1.0")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--layouts", default="dense,sampled")
     args = ap.parse_args()
     from paper_2205_06619_b200 import _ext
     try:
@@ -37,11 +43,14 @@ def main():
     for m in (int(x) for x in args.sizes.split(",")):
         for r in (int(x) for x in args.ranks.split(",")):
             for d in (float(x) for x in args.density.split(",")):
-                res = _ext.bench_maxplus(m, m, r, d, seed=7, reps=args.reps, flush_l2=True)
-                line = {"config": f"c5 m=n={m} r={r} density={d}", "m": m, "n": m, "rank": r, "density": d,
+              for lay in args.layouts.split(","):
+                res = _ext.bench_maxplus(m, m, r, d, seed=7, reps=args.reps, flush_l2=True, layout=lay)
+                line = {"config": f"c5 m=n={m} r={r} density={d}", "layout": res["layout"], "m": m, "n": m,
+                        "rank": r, "density": d, "algorithmic_bytes": res["bytes"],
                         "avg_ms": res["avg_ms"], "best_ms": res["best_ms"], "given": int(res["given"]),
                         "objective": res["objective"],
                         "hbm": {"achieved_gbs": res["gbs"], "peak_gbs": hbm, "frac": res["gbs"] / hbm},
+                        # computed (entry, k) pairs: every entry (dense) or the given ones (sampled)
                         "alu": {"achieved_gpairs": res["gpairs_per_s"], "peak_gpairs": alu_peak,
                                 "frac": res["gpairs_per_s"] / alu_peak},
                         "useful_gentries_per_s": res["given"] / (res["avg_ms"] * 1e-3) / 1e9}

@@ -140,6 +140,9 @@ int stmf_set_max_attempts(stmf_session* s, int64_t max_attempts);
  * the product caches are rebuilt from the factors and the objective is recomputed from
  * scratch, and it must equal the error the fit carries (STMF_ERR_AUDIT otherwise). */
 int stmf_set_audit(stmf_session* s, int on);
+/* Communicator of a sharded session: out3 = {ranks, this rank, kind}, kind 1 = NCCL
+ * (ncclCommCount / ncclCommUserRank), 0 = in-process group, -1 = not sharded. */
+int stmf_comm_info(stmf_session* s, int* out3);
 
 /* ---- the reference's other fit methods ---- */
 

@@ -138,6 +138,7 @@ def lib():
         "stmf_replayed_sweeps": [_vp, ctypes.POINTER(_i64)],
         "stmf_set_max_attempts": [_vp, _i64],
         "stmf_set_audit": [_vp, _int],
+        "stmf_comm_info": [_vp, _vp],
         "stmf_b_norm": [_i64, _vp, _int, ctypes.POINTER(_dbl)],
     }
     for name, args in sig.items():
@@ -157,7 +158,7 @@ EXPORTED_SYMBOLS = ["stmf_last_error", "stmf_version", "stmf_create", "stmf_dest
                     "stmf_set_strategy", "stmf_row_scores", "stmf_matrix_candidates",
                     "stmf_masked_rmse", "stmf_distance_correlation", "stmf_csv_open", "stmf_csv_fill",
                     "stmf_csv_close", "stmf_release_memory",
-                    "stmf_trajectory", "stmf_replayed_sweeps", "stmf_set_max_attempts", "stmf_set_audit",
+                    "stmf_trajectory", "stmf_replayed_sweeps", "stmf_set_max_attempts", "stmf_set_audit", "stmf_comm_info",
                     "stmf_b_norm"]
 
 # include/stmf_b200.h: families and ByRow selection rules
@@ -338,7 +339,7 @@ class Session:
         counts = np.zeros(8, np.int64)
         bs = -1 if budget_sweeps is None else int(budget_sweeps)
         secs = 0.0 if budget_seconds is None else float(budget_seconds)
-        if traj_cap is None and not self.sharded:
+        if traj_cap is None:
             _check(lib().stmf_run(self._h, bs, secs, float(epsilon), None, None, 0, _p(counts)))
             L = int(counts[0])
             tt = np.empty(L, np.float64)
@@ -368,6 +369,14 @@ class Session:
         """Stop later runs after exactly `cap` attempts (0 = no cap): the checker's
         oracle.fit(max_attempts=...) on the device (host-driven sweep loop)."""
         _check(lib().stmf_set_max_attempts(self._h, int(cap)))
+
+    def comm_info(self) -> dict:
+        """Sharded sessions: the communicator's rank count and this rank (NCCL:
+        ncclCommCount / ncclCommUserRank); kind "nccl", "local" or "none"."""
+        out = np.zeros(3, np.int32)
+        _check(lib().stmf_comm_info(self._h, _p(out)))
+        return {"nranks": int(out[0]), "rank": int(out[1]),
+                "kind": {1: "nccl", 0: "local", -1: "none"}[int(out[2])]}
 
     def set_audit(self, on: bool = True):
         """RunConfig.audit: after every sweep the caches are rebuilt and the objective

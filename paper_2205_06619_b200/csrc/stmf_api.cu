@@ -211,6 +211,8 @@ struct SessionBase {
   // test hook mirroring oracle.fit(max_attempts=...): stop after that many attempts
   virtual void set_max_attempts(int64_t) { fail(STMF_ERR_INVALID, "attempt caps are single-device only"); }
   virtual void set_audit(int) { fail(STMF_ERR_INVALID, "audit mode is single-device only"); }
+  // sharded sessions: {ranks, this rank, kind (0 in-process group, 1 NCCL)} from the communicator
+  virtual void comm_info(int* out3) { out3[0] = 1; out3[1] = 0; out3[2] = -1; }
   // the reference's other fit methods
   virtual void set_strategy(int family, int selection) {
     if (family != STMF_FAMILY_BYROW || selection != STMF_SEL_TD_A)
@@ -2939,6 +2941,12 @@ int stmf_replayed_sweeps(stmf_session* s, int64_t* n) {
 int stmf_set_max_attempts(stmf_session* s, int64_t max_attempts) {
   NEED(s);
   GUARD(s->impl->set_max_attempts(max_attempts));
+}
+
+int stmf_comm_info(stmf_session* s, int* out3) {
+  NEED(s);
+  if (!out3) return set_err(STMF_ERR_INVALID, "null argument");
+  GUARD(s->impl->comm_info(out3));
 }
 
 int stmf_set_audit(stmf_session* s, int on) {

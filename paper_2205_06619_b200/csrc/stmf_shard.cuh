@@ -86,12 +86,13 @@ template <typename T>
 __global__ void k_pack_row(int64_t nc, int rank, int64_t ml, int64_t il, const int32_t* __restrict__ cols,
                            const T* __restrict__ x, const uint8_t* __restrict__ ag, const T* __restrict__ Ut,
                            int32_t* __restrict__ pcols, T* __restrict__ px, int32_t* __restrict__ prowhist,
-                           T* __restrict__ purow) {
+                           T* __restrict__ purow, uint8_t* __restrict__ pag) {
   for (int l = threadIdx.x; l < rank; l += blockDim.x) prowhist[l] = 0;
   __syncthreads();
   for (int64_t p = threadIdx.x; p < nc; p += blockDim.x) {
     pcols[p] = cols[p];
     px[p] = x[p];
+    pag[p] = ag[p];
     atomicAdd(&prowhist[ag[p]], 1);
   }
   for (int l = threadIdx.x; l < rank; l += blockDim.x) purow[l] = Ut[(int64_t)l * ml + il];
@@ -150,6 +151,9 @@ struct Comm {
   virtual void broadcast(std::vector<void*>& b, size_t bytes, int root, cudaStream_t st) = 0;
   virtual int world() = 0;
   virtual int first_shard() = 0;  // global index of local shard 0
+  // ranks / this rank as the communicator reports them (NCCL: ncclCommCount /
+  // ncclCommUserRank; the in-process group: its shard count / 0); kind 0 local, 1 NCCL
+  virtual void info(int* nranks, int* me, int* kind) { *nranks = world(); *me = first_shard(); *kind = 0; }
 };
 
 struct LocalComm : Comm {
@@ -203,6 +207,8 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   bool ok = false;
   static NcclApi& get() {
     static NcclApi a;
@@ -216,6 +222,8 @@ struct NcclApi {
       a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
       a.Broadcast = (decltype(a.Broadcast))dlsym(h, "ncclBroadcast");
       a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+      a.CommCount = (decltype(a.CommCount))dlsym(h, "ncclCommCount");
+      a.CommUserRank = (decltype(a.CommUserRank))dlsym(h, "ncclCommUserRank");
       if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.AllGather || !a.Broadcast)
         fail(STMF_ERR_NCCL, "libnccl.so.2 lacks required symbols");
       a.ok = true;
@@ -246,6 +254,12 @@ struct NcclComm : Comm {
   int nlocal() override { return 1; }
   int world() override { return W; }
   int first_shard() override { return R; }
+  void info(int* nranks, int* me, int* kind) override {
+    if (!NcclApi::get().CommCount || !NcclApi::get().CommUserRank) fail(STMF_ERR_NCCL, "libnccl lacks ncclCommCount");
+    NCK(NcclApi::get().CommCount(comm, nranks));
+    NCK(NcclApi::get().CommUserRank(comm, me));
+    *kind = 1;
+  }
   void min_f32(std::vector<float*>& b, size_t count, cudaStream_t st) override {
     if (count) NCK(NcclApi::get().AllReduce(b[0], b[0], count, ncclFloat32, ncclMin, comm, st));
   }
@@ -292,7 +306,7 @@ struct Shard {
   DevBuf<uint8_t> rowbuf;
   DevBuf<u64> ckeys, ckeys2;
   DevBuf<int32_t> cvals, cperm, cj, ck;
-  DevBuf<T> cx, xrow_dense;
+  DevBuf<T> cx, xrow_dense, cmi;
   DevBuf<T> vbuf, ubufA, ubufB, vbufB, dtmpA, dtmpB;
   DevBuf<u64> acc;
   DevBuf<int64_t> limbs;
@@ -338,7 +352,13 @@ struct ShardGroup : SessionBase {
   int unroll = getenv("STMF_UNROLL") ? atoi(getenv("STMF_UNROLL")) : 2;
   int64_t long_thr = getenv("STMF_LONG") ? atoll(getenv("STMF_LONG")) : 4096;
   int group_major = 0;
-  size_t off_x = 0, off_h = 0, off_u = 0, rowbuf_bytes = 0;
+  size_t off_x = 0, off_h = 0, off_u = 0, off_ag = 0, rowbuf_bytes = 0;
+  // adaptive speculation (as the single-device engine): the first batch of a row
+  // covers scale x the candidates the row consumed on its previous visit (+ add),
+  // floored by batch_floor; later batches grow by `growth`
+  std::vector<int64_t> row_depth;
+  int batch_floor = 1, sched_add = 1;
+  double sched_scale = 0.9, sched_growth = 1.5;
   int gridX = -1000;
 
   ~ShardGroup() override {
@@ -392,7 +412,13 @@ struct ShardGroup : SessionBase {
     off_x = ((size_t)4 * n + 15) / 16 * 16;
     off_h = (off_x + sizeof(T) * n + 15) / 16 * 16;
     off_u = (off_h + 4 * (size_t)rank + 15) / 16 * 16;
-    rowbuf_bytes = off_u + sizeof(T) * rank;
+    off_ag = (off_u + sizeof(T) * rank + 15) / 16 * 16;
+    rowbuf_bytes = off_ag + (size_t)n;
+    batch_floor = (int)std::max<int64_t>(1, std::min<int64_t>(128, 8000000 / std::max<int64_t>(N, 1)));
+    if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.5; }
+    if (const char* e = getenv("STMF_SCHED")) sscanf(e, "%lf,%d,%lf", &sched_scale, &sched_add, &sched_growth);
+    row_depth.assign(m, 0);
     const T* Xp = X_rows;
     const uint8_t* Mp = mask_rows;
     int first = c->first_shard();
@@ -489,7 +515,7 @@ struct ShardGroup : SessionBase {
     s.gm1.alloc((size_t)W * n); s.gm2.alloc((size_t)W * n); s.ga1.alloc((size_t)W * n);
     s.rowbuf.alloc(rowbuf_bytes);
     s.ckeys.alloc(n); s.ckeys2.alloc(n); s.cvals.alloc(n); s.cperm.alloc(n);
-    s.cj.alloc(n); s.ck.alloc(n); s.cx.alloc(n); s.xrow_dense.alloc(n);
+    s.cj.alloc(n); s.ck.alloc(n); s.cx.alloc(n); s.xrow_dense.alloc(n); s.cmi.alloc((size_t)rank * n);
     s.vbuf.alloc((size_t)Emax * n); s.vbufB.alloc((size_t)Emax * n);
     s.ubufA.alloc((size_t)Emax * ml); s.ubufB.alloc((size_t)Emax * ml);
     s.dtmpA.alloc(ml); s.dtmpB.alloc(n);
@@ -548,6 +574,7 @@ struct ShardGroup : SessionBase {
     }
     CK(cudaStreamSynchronize(st));
     sync_factor_copies(-1);
+    std::fill(row_depth.begin(), row_depth.end(), 0);  // a new state: no speculation history
     have_factors = true;
     dirty = true;
     cache_k = -1;
@@ -690,7 +717,8 @@ struct ShardGroup : SessionBase {
       int64_t beg = o->h_row_ptr[il];
       k_pack_row<T><<<1, 256, 0, st>>>(nc, rank, o->ml, il, o->col_idx.p + beg, o->xr.p + beg, o->agr.p + beg,
                                        o->Ut.p, (int32_t*)o->rowbuf.p, (T*)(o->rowbuf.p + off_x),
-                                       (int32_t*)(o->rowbuf.p + off_h), (T*)(o->rowbuf.p + off_u));
+                                       (int32_t*)(o->rowbuf.p + off_h), (T*)(o->rowbuf.p + off_u),
+                                       o->rowbuf.p + off_ag);
       LAUNCH_CK();
     }
     std::vector<void*> rb;
@@ -700,6 +728,19 @@ struct ShardGroup : SessionBase {
       Shard<T>& s = *sp;
       const int32_t* cols = (const int32_t*)s.rowbuf.p;
       const T* xrow = (const T*)(s.rowbuf.p + off_x);
+      if (nc <= 4 * kCandThreads && rank <= 256) {
+        // one block ranks the candidates (stable merge sort on the score keys), votes
+        // and fills the dense row, as in the single-device engine; the extra blocks
+        // of the launch fill CM^(-i) (not needed here, but the kernel's contract)
+        auto kern = nc <= kCandThreads ? k_cand_row<T, 1> : k_cand_row<T, 4>;
+        int64_t need = ((int64_t)rank * n + kCandThreads - 1) / kCandThreads;
+        unsigned grid = (unsigned)(1 + std::max<int64_t>(1, std::min<int64_t>(need, nsm)));
+        kern<<<grid, kCandThreads, 0, st>>>((int)nc, n, rank, cols, xrow, s.rowbuf.p + off_ag, s.score.p,
+                                            s.colhist.p, s.cj.p, s.ck.p, s.cx.p, s.xrow_dense.p, i, s.cm1.p, s.cm2.p,
+                                            s.cmarg.p, s.cmi.p, nullptr, nullptr, 0);
+        LAUNCH_CK();
+        continue;
+      }
       k_cand_keys<<<nblk(nc, 256), 256, 0, st>>>(nc, cols, s.score.p, s.ckeys.p, s.cvals.p);
       LAUNCH_CK();
       size_t bytes = s.cubtmp_bytes;
@@ -799,6 +840,17 @@ struct ShardGroup : SessionBase {
     double* tt; double* te; int64_t cap, len;
     int64_t attempts, accepts, visits, evaluated;
   };
+  // null trajectory buffers: the trajectory is kept here (growable), read back with
+  // stmf_trajectory (as single-device sessions)
+  std::vector<double> tj_t, tj_e;
+  void trajectory(double* t, double* e, int64_t cap, int64_t* len) override {
+    *len = (int64_t)tj_t.size();
+    if (!t || !e) return;
+    if (cap < *len) fail(STMF_ERR_CAPACITY, "trajectory has %lld samples, capacity %lld", (long long)*len,
+                         (long long)cap);
+    std::memcpy(t, tj_t.data(), sizeof(double) * tj_t.size());
+    std::memcpy(e, tj_e.data(), sizeof(double) * tj_e.size());
+  }
   double run_now(RunState& R) { return R.wall ? now_s() - R.t0 : (double)R.cur_sweep; }
   bool out_of_time(RunState& R) {
     // every rank must take the same branch: agree on the wall-clock decision
@@ -807,6 +859,12 @@ struct ShardGroup : SessionBase {
     return v != 0;
   }
   void traj_append(RunState& R, double t, double e) {
+    if (!R.tt) {
+      tj_t.push_back(t);
+      tj_e.push_back(e);
+      R.len++;
+      return;
+    }
     if (R.len >= R.cap) fail(STMF_ERR_CAPACITY, "trajectory capacity %lld exceeded", (long long)R.cap);
     R.tt[R.len] = t; R.te[R.len] = e; R.len++;
   }
@@ -817,10 +875,13 @@ struct ShardGroup : SessionBase {
     R.visits++;
     std::vector<int> hk;
     int64_t t0 = 0;
-    size_t bi = 0;
+    // the same decisions on every rank, so the same schedule
+    int next = row_depth[i] > 0 ? (int)std::max<int64_t>(batch_floor, std::min<int64_t>(
+                                      Emax, (int64_t)(sched_scale * row_depth[i]) + sched_add))
+                                : batch_sched[0];
     while (t0 < nc) {
-      int E = (int)std::min<int64_t>(nc - t0, batch_sched[std::min(bi, batch_sched.size() - 1)]);
-      bi++;
+      int E = (int)std::min<int64_t>(nc - t0, next);
+      next = std::min(Emax, std::max(next + 1, (int)(next * sched_growth)));
       eval_batch(i, t0, E);
       hk.resize(E);
       CK(cudaMemcpyAsync(hk.data(), sh[0]->ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
@@ -835,6 +896,7 @@ struct ShardGroup : SessionBase {
             commit(op, q, hk[q]);
             err = f;
             R.accepts++;
+            row_depth[i] = t0 + q + 1;
             traj_append(R, run_now(R), err);
             return;
           }
@@ -842,13 +904,14 @@ struct ShardGroup : SessionBase {
       if (out_of_time(R)) return;
       t0 += E;
     }
+    row_depth[i] = nc;
   }
 
   void run(int64_t budget_sweeps, double budget_seconds, double epsilon, double* tt, double* te, int64_t cap,
            int64_t* counts) override {
     if (budget_sweeps < 0 && !(budget_seconds > 0)) fail(STMF_ERR_INVALID, "set budget_sweeps or budget_seconds");
-    if (!tt || !te) fail(STMF_ERR_INVALID, "sharded sessions need trajectory buffers");
     RunState R{};
+    if (!tt) { tj_t.clear(); tj_e.clear(); }
     R.wall = budget_seconds > 0;
     R.budget_seconds = budget_seconds;
     R.t0 = now_s();
@@ -890,6 +953,7 @@ struct ShardGroup : SessionBase {
   void bench_product(int, int, double*, double*) override { fail(STMF_ERR_INVALID, "not available on sharded sessions"); }
   void* stream() override { return (void*)st; }
   int device_id() const override { return dev; }
+  void comm_info(int* out3) override { comm->info(&out3[0], &out3[1], &out3[2]); }
   void set_profiling(int) override {}
   void counters(int64_t* out) override {
     for (int i = 0; i < 8; i++) out[i] = 0;

@@ -101,6 +101,7 @@ def test_sharded_world1_over_a_real_nccl_communicator(seed, m, n, r, frac, sweep
     nnz = work.mask.sum(axis=1)
     s = _ext.Session.sharded(work.values, work.mask, r, work.m, np.array([0, work.m]), nnz, 1, 0, _nccl_id())
     try:
+        assert s.comm_info() == {"nranks": 1, "rank": 0, "kind": "nccl"}
         s.set_factors(U0)
         tt, te, c = s.run(budget_sweeps=sweeps, epsilon=0.0)
         U, V = s.get_factors()
