@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu", "stmf_io.cc"]
 HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh",
-           "stmf_metrics.cuh"]
+           "stmf_metrics.cuh", "stmf_fast1.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -59,9 +59,18 @@ def nccl_include() -> str:
     raise RuntimeError("nccl.h not found")
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+CHECKED_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libstmf_b200_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(),
+          checked: bool = False) -> str:
     """Compile csrc/*.cu into lib/libstmf_b200.so for sm_100a (in-tree).  ``out`` /
-    ``defines``: an experiment variant of the library (loaded with STMF_LIB)."""
+    ``defines``: an experiment variant of the library (loaded with STMF_LIB).
+    ``checked``: lib/libstmf_b200_checked.so with device-side index range checks
+    (STMF_CHECKS; load it with STMF_LIB)."""
+    if checked:
+        out = out or CHECKED_LIB_PATH
+        defines = tuple(defines) + ("STMF_CHECKS",)
     out = out or LIB_PATH
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "stmf_b200.h")]

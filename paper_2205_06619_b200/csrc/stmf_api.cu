@@ -34,6 +34,7 @@
 #include "stmf_strategies.cuh"
 #include "stmf_metrics.cuh"
 #include "stmf_graph.cuh"
+#include "stmf_fast1.cuh"
 
 using namespace stmf;
 
@@ -412,6 +413,119 @@ struct Session : SessionBase {
     }
     return sa;
   }
+  // phase B's first half from per-line statistics (stmf_fast1.cuh); STMF_FAST1=0: full passes
+  // off by default: measured slower at configs 2 and 3 (profiles/r02_fast1.md: the walks fall
+  // back to the full pass for 22-30% of (eval, line) pairs at config 3's density)
+  bool fast1 = getenv("STMF_FAST1") ? atoi(getenv("STMF_FAST1")) != 0 : false;
+  DevBuf<T> f1_uv, f1_ux, f1_rv, f1_rx;
+  DevBuf<int32_t> f1_uo, f1_ro;
+  DevBuf<int> f1_k, f1_valid;  // F-ULF statistics' k; F-URF per-k validity
+  bool f1_row_ready = false;   // host loop: the F-ULF statistics belong to the current row visit
+  DevBuf<unsigned long long> f1_diag;  // STMF_FAST1_STATS: walk / fallback counts (stderr at the end of run)
+  Fast1<T> fast1_bufs(const int32_t* cjp) {
+    Fast1<T> F1{};
+    F1.stats = f1_diag.p;  // allocated at init under STMF_FAST1_STATS
+    F1.ulf = TopK<T>{f1_uv.p, f1_uo.p, f1_ux.p};
+    F1.ulf_k = f1_k.p;
+    F1.urf = TopK<T>{f1_rv.p, f1_ro.p, f1_rx.p};
+    F1.urf_valid = f1_valid.p;
+    F1.rm1 = rm1.p;
+    F1.rmarg = rmarg.p;
+    F1.cj = cjp;
+    return F1;
+  }
+  // the line statistics of a row visit: F-ULF w.r.t. CM^(-i)_k and (if stale) F-URF
+  // w.r.t. RM_k, k = the factor index of the row's first candidate (ck[0])
+  void fast1_row_stats(cudaStream_t s_) {
+    k_top_lines<T><<<warps_grid(m), 256, 0, s_>>>(m, row_ptr.p, col_idx.p, xr.p, cmi.p, n, ck.p, nullptr,
+                                                   TopK<T>{f1_uv.p, f1_uo.p, f1_ux.p}, 0);
+    k_top_mark<<<1, 1, 0, s_>>>(ck.p, nullptr, f1_k.p);
+    k_top_lines<T><<<warps_grid(n), 256, 0, s_>>>(n, col_ptr.p, row_idx.p, xc.p, rm1.p, m, ck.p, f1_valid.p,
+                                                   TopK<T>{f1_rv.p, f1_ro.p, f1_rx.p}, (int64_t)kTop * n);
+    k_top_mark<<<1, 1, 0, s_>>>(ck.p, f1_valid.p, nullptr);
+  }
+  // diagnostics (STMF_FAST1_CHECK): the statistics walk's line values against full passes
+  void fast1_check(SideB<T> sa, SideB<T> sb, int E, const int32_t* bk, const int32_t* bj, int64_t i) {
+    DevBuf<T> oa, ob;
+    DevBuf<int> zero;
+    oa.alloc((size_t)E * m); ob.alloc((size_t)E * n); zero.alloc(rank + 1);
+    CK(cudaMemsetAsync(zero.p, 0, sizeof(int) * rank, st));
+    int neg = -2;
+    CK(cudaMemcpyAsync(zero.p + rank, &neg, sizeof(int), cudaMemcpyHostToDevice, st));
+    SideB<T> a2 = sa, b2 = sb;
+    a2.out = oa.p; b2.out = ob.p;
+    Fast1<T> F1 = fast1_bufs(bj);
+    F1.ulf_k = zero.p + rank;
+    F1.urf_valid = zero.p;
+    int ng = (E + kEG - 1) / kEG;
+    k_pass1_fast<T><<<warps_grid((m + n) * ng), 256, 0, st>>>(a2, b2, E, bk, F1);
+    LAUNCH_CK();
+    std::vector<T> fa((size_t)E * m), fb((size_t)E * n), ga((size_t)E * m), gb((size_t)E * n);
+    CK(cudaMemcpyAsync(fa.data(), sa.out, sizeof(T) * fa.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fb.data(), sb.out, sizeof(T) * fb.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ga.data(), oa.p, sizeof(T) * ga.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(gb.data(), ob.p, sizeof(T) * gb.size(), cudaMemcpyDeviceToHost, st));
+    int hk = -1;
+    CK(cudaMemcpyAsync(&hk, f1_k.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    std::vector<int> hv(rank), hks(E);
+    CK(cudaMemcpyAsync(hv.data(), f1_valid.p, sizeof(int) * rank, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hks.data(), bk, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
+    ssync();
+    int bad = 0;
+    for (size_t t = 0; t < fa.size(); t++)
+      if (!(fa[t] == ga[t]) && bad++ < 5)
+        fprintf(stderr, "[fast1 check] row %lld ULF eval %zu line %zu k %d (ulf_k %d): fast %.17g full %.17g\n",
+                (long long)i, t / m, t % m, hks[t / m], hk, (double)fa[t], (double)ga[t]);
+    for (size_t t = 0; t < fb.size(); t++)
+      if (!(fb[t] == gb[t]) && bad++ < 10)
+        fprintf(stderr, "[fast1 check] row %lld URF eval %zu line %zu k %d (valid %d): fast %.17g full %.17g\n",
+                (long long)i, t / n, t % n, hks[t / n], hv[hks[t / n]], (double)fb[t], (double)gb[t]);
+    if (bad) fprintf(stderr, "[fast1 check] row %lld: %d mismatches\n", (long long)i, bad);
+    // details of the first ULF mismatch: the row's entries, the base, the statistics
+    for (size_t t = 0; t < fa.size(); t++) {
+      if (fa[t] == ga[t]) continue;
+      int q = (int)(t / m);
+      int64_t L = (int64_t)(t % m);
+      int k = hks[q];
+      int64_t b0 = h_row_ptr[L], b1 = h_row_ptr[L + 1];
+      std::vector<int32_t> cols(b1 - b0);
+      std::vector<T> xs(b1 - b0), base(n), xrd(n), st4v(kTop * m), st4x(kTop * m);
+      std::vector<int32_t> st4o(kTop * m);
+      T sqv;
+      CK(cudaMemcpyAsync(cols.data(), col_idx.p + b0, 4 * cols.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(xs.data(), xr.p + b0, sizeof(T) * xs.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(base.data(), cmi.p + (size_t)k * n, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(xrd.data(), xrow_dense.p, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(st4v.data(), f1_uv.p, sizeof(T) * st4v.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(st4x.data(), f1_ux.p, sizeof(T) * st4x.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(st4o.data(), f1_uo.p, 4 * st4o.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&sqv, sq.p + q, sizeof(T), cudaMemcpyDeviceToHost, st));
+      ssync();
+      T best = INFINITY;
+      size_t bp = 0;
+      std::vector<std::pair<T, int>> bt;
+      for (size_t e = 0; e < cols.size(); e++) {
+        int c = cols[e];
+        T b = base[c];
+        T vn = std::min(b, (T)(xrd[c] - sqv));
+        T term = xs[e] - vn;
+        if (term < best) { best = term; bp = e; }
+        bt.push_back({(T)(xs[e] - b), c});
+      }
+      std::sort(bt.begin(), bt.end());
+      fprintf(stderr, "[fast1 detail] line %lld eval %d k %d: host full min %.17g at col %d (x %.17g b %.17g xr %.17g)\n",
+              (long long)L, q, k, (double)best, cols[bp], (double)xs[bp], (double)base[cols[bp]], (double)xrd[cols[bp]]);
+      for (int u = 0; u < 4 && u < (int)bt.size(); u++)
+        fprintf(stderr, "  host top %d: val %.17g col %d | dev slot %d: val %.17g col %d x %.17g\n", u,
+                (double)bt[u].first, bt[u].second, u, (double)st4v[u * m + L], st4o[u * m + L], (double)st4x[u * m + L]);
+      break;
+    }
+  }
+  void fast1_invalidate(int k) {  // k < 0: every k
+    if (!fast1) return;
+    if (k < 0) CK(cudaMemsetAsync(f1_valid.p, 0, sizeof(int) * rank, st));
+    else CK(cudaMemsetAsync(f1_valid.p + k, 0, sizeof(int), st));
+  }
   // batch scratch
   int Emax = 512;
   DevBuf<T> vbuf, ubufB, ubufA, vbufB, dtmpA, dtmpB;
@@ -627,6 +741,17 @@ struct Session : SessionBase {
     cj.alloc(std::max<int64_t>(n, Emax)); ck.alloc(std::max<int64_t>(n, Emax));
     cx.alloc(std::max<int64_t>(n, Emax)); xrow_dense.alloc(n);
     cmi.alloc((size_t)rank * n); sq.alloc(n);
+    if (fast1) {
+      f1_uv.alloc((size_t)kTop * m); f1_ux.alloc((size_t)kTop * m); f1_uo.alloc((size_t)kTop * m);
+      f1_rv.alloc((size_t)rank * kTop * n); f1_rx.alloc((size_t)rank * kTop * n); f1_ro.alloc((size_t)rank * kTop * n);
+      f1_k.alloc(1); f1_valid.alloc(rank);
+      if (getenv("STMF_FAST1_STATS")) {
+        f1_diag.alloc(4);
+        CK(cudaMemsetAsync(f1_diag.p, 0, 32, st));
+      }
+      CK(cudaMemsetAsync(f1_valid.p, 0, sizeof(int) * rank, st));
+      CK(cudaMemsetAsync(f1_k.p, 0xff, sizeof(int), st));
+    }
 
     if (split_ulf) {
       hp_idx.alloc(N); hp_x.alloc(N); hp_t1.alloc(N); hp_t2.alloc(N); hp_ag.alloc(N); hp_split.alloc(m);
@@ -725,6 +850,7 @@ struct Session : SessionBase {
     if ((int64_t)row_depth.size() == m) std::fill(row_depth.begin(), row_depth.end(), 0);
     rdepth_on_dev = false;
     depth_ema = 0;
+    fast1_invalidate(-1);
     have_factors = true;
     cur_valid = false;
     dirty = true;
@@ -1144,7 +1270,20 @@ struct Session : SessionBase {
     SideB<T> sa = side_ulf(acc_ulf, chg_ulf);
     SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, acc_urf, chg_urf,
                 0, long_thr, group_major};
-    if (profiling) CK(cudaEventRecord(ev_b0, st));
+    if (profiling && !getenv("STMF_TIME_B_ONLY")) CK(cudaEventRecord(ev_b0, st));
+    if (fast1 && f1_row_ready) {
+      // both second residuations from the line statistics (+ the rmarg == j scatter),
+      // then phase B's error pass reads them (mode 2)
+      k_pass1_fast<T><<<warps_grid((m + n) * ng), 256, 0, st>>>(sa, sb, E, bk, fast1_bufs(bj));
+      LAUNCH_CK();
+      k_pass1_dscatter<T><<<warps_grid((int64_t)E * ((m + 31) / 32)), 256, 0, st>>>(
+          m, n, row_ptr.p, col_idx.p, xr.p, E, bk, bj, rmarg.p, f1_valid.p, ubufA.p, vbufB.p);
+      LAUNCH_CK();
+      if (getenv("STMF_FAST1_CHECK")) fast1_check(sa, sb, E, bk, bj, i);
+      sa.mode = 2;
+      sb.mode = 2;
+    }
+    if (profiling && getenv("STMF_TIME_B_ONLY")) CK(cudaEventRecord(ev_b0, st));
     launch_phaseB<T>(unroll, warps_grid((m + n) * ng), st, sa, sb, E, bk, flags.p, F, exact_limit, long_rows.p,
                      n_long_rows, long_cols.p, n_long_cols, nsm);
     LAUNCH_CK();
@@ -1266,6 +1405,7 @@ struct Session : SessionBase {
     cache_k = dirty ? -1 : k;  // incremental cache update iff only this index changed
     dirty = true;
     stats_dirty[k] = 1;
+    fast1_invalidate(k);
   }
 
   // ---- run_fit sweep loop ----------------------------------------------------------
@@ -1378,6 +1518,14 @@ struct Session : SessionBase {
     ensure_caches();
     ph_mark(0);
     int64_t nc = build_candidates(i);
+    if (fast1 && selection != STMF_SEL_TD_B) {
+      fast1_row_stats(st);
+      f1_row_ready = true;
+    }
+    struct RowDone {
+      bool& r;
+      ~RowDone() { r = false; }
+    } row_done{f1_row_ready};
     ph_mark(1);
     R.visits++;
     std::vector<int> hk;
@@ -1825,6 +1973,7 @@ struct Session : SessionBase {
     }
     B.beta = beta_rel;
     B.aval = d_aval.p;
+    B.urf_valid = fast1 ? f1_valid.p : nullptr;
     return B;
   }
 
@@ -1886,6 +2035,7 @@ struct Session : SessionBase {
                                        selection == STMF_SEL_TD ? 1 : 0);
     }
     row_partition();
+    if (fast1) fast1_row_stats(st);
     dr = cap_end(b_row);
     cudaGraph_t b_batch = add_cond(b_row, dr, h_batch, cudaGraphCondTypeWhile);
 
@@ -1906,6 +2056,13 @@ struct Session : SessionBase {
       SideB<T> sa = side_ulf(nullptr, nullptr);
       SideB<T> sb{n, col_ptr.p, row_idx.p, xc.p, t1c.p, t2c.p, agc.p, ubufA.p, m, V.p, vbufB.p, nullptr, nullptr,
                   0, long_thr, group_major};
+      if (fast1) {
+        k_pass1_fast<T><<<(unsigned)nsm * 8, 256, 0, st>>>(sa, sb, 0, nullptr, fast1_bufs(cj.p), c, ck.p);
+        k_pass1_dscatter<T><<<(unsigned)nsm * 4, 256, 0, st>>>(m, n, row_ptr.p, col_idx.p, xr.p, 0, nullptr, nullptr,
+                                                               rmarg.p, f1_valid.p, ubufA.p, vbufB.p, c, ck.p, cj.p);
+        sa.mode = 2;
+        sb.mode = 2;
+      }
       // one wave of resident CTAs (the kernel's launch bounds)
       unsigned gb = (unsigned)nsm * (unroll >= 4 ? 2 : sizeof(T) == 4 ? kPhaseBCtasF32 : unroll > 1 ? 2 : kPhaseBCtasF64);
       if (unroll >= 4)
@@ -2090,8 +2247,8 @@ struct Session : SessionBase {
         phaseB_timed += h.batches;
       }
       // kernel nodes executed: row (3), batch (5 + tick), escalation round (7 + 1), accept (6, +7 fp64)
-      g_launches += h.visits * 3 + h.batches * (5 + (graph_prof ? 1 : 0)) + h.esc_rounds * 8 +
-                    h.accepts * (kExact ? 6 : 13);
+      g_launches += h.visits * (3 + (fast1 ? 4 : 0)) + h.batches * (5 + (graph_prof ? 1 : 0) + (fast1 ? 2 : 0)) +
+                    h.esc_rounds * 8 + h.accepts * (kExact ? 6 : 13);
       if (getenv("STMF_GRAPH_STATS"))
         fprintf(stderr,
                 "[stmf graph] rows %lld batches %lld esc_rounds %lld accepts %lld | sweep %.2f ms: phaseB %.2f "
@@ -2196,6 +2353,12 @@ struct Session : SessionBase {
     ph_report();
     counts[4] = R.visits; counts[5] = R.evaluated; counts[6] = n_escalations - esc0;
     counts[7] = n_product_passes - pp0;
+    if (f1_diag.p) {
+      unsigned long long d[4];
+      CK(cudaMemcpy(d, f1_diag.p, 32, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[fast1 stats] ULF evals x lines %llu, fallbacks %llu (%.2f%%); URF %llu, fallbacks %llu (%.2f%%)\n",
+              d[0], d[1], 100.0 * d[1] / std::max(d[0], 1ull), d[2], d[3], 100.0 * d[3] / std::max(d[2], 1ull));
+    }
   }
 
   // ---- diff-test hooks -----------------------------------------------------------

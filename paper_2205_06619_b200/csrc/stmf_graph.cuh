@@ -57,6 +57,7 @@ struct GBufs {
   int exact;
   double dr[2], da[2], beta;  // fp64 decision bound (Session::margin_of)
   double* aval;               // the batch's eval objectives (fixed point -> binary64), 2 Emax
+  int* urf_valid;             // per-k validity of the F-URF line statistics (stmf_fast1.cuh); may be null
 };
 
 __device__ __forceinline__ int grow_next(const DevCtl* c, int next) {
@@ -383,6 +384,7 @@ __global__ void k_g_commit(DevCtl* c, GBufs<T> B, T* __restrict__ Ut, T* __restr
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c->cache_k = k;
     c->accepts++;
+    if (B.urf_valid) B.urf_valid[k] = 0;  // row k of V changes: its F-URF statistics too
   }
 }
 

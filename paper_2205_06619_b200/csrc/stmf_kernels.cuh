@@ -24,6 +24,25 @@ namespace stmf {
 
 typedef unsigned long long u64;
 
+// Checked build (STMF_CHECKS, _ext.build(checked=True) -> lib/libstmf_b200_checked.so):
+// every gathered index is range-checked on the device and a violation traps with the
+// kernel's file:line (a stand-in for compute-sanitizer, which this pool does not run).
+#ifdef STMF_CHECKS
+#include <cstdio>
+#define STMF_IDX(i, n)                                                                              \
+  do {                                                                                            \
+    if ((unsigned long long)(long long)(i) >= (unsigned long long)(long long)(n)) {               \
+      printf("stmf check failed %s:%d: index %lld not in [0, %lld)\n", __FILE__, __LINE__,         \
+             (long long)(i), (long long)(n));                                                     \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define STMF_IDX(i, n) \
+  do {                 \
+  } while (0)
+#endif
+
 struct U64Less {
   __device__ __forceinline__ bool operator()(u64 a, u64 b) const { return a < b; }
 };
@@ -391,6 +410,8 @@ __global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const i
   if (kdev) k = *kdev;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = rowof[p], c = colof[p];
+    STMF_IDX(r, m);
+    STMF_IDX(c, n);
     T b1, b2;
     int a1, a2;
     if (k < 0) {
@@ -1092,6 +1113,7 @@ __device__ __forceinline__ void pass1_seg(const SideB<T>& S, const typename Vec1
       bool ok = p < hi;
       x[u] = ok ? xv[p] : tinf<T>();
       c[u] = ok ? idx[p] : 0;
+      STMF_IDX(c[u], S.len_other);
     }
     if (SHARED) {
 #pragma unroll
@@ -1127,6 +1149,7 @@ __device__ __forceinline__ void pass2_seg(const SideB<T>& S, const typename Vec1
       int pp = ok ? p : lo;
       x[u] = xv[pp];
       c[u] = idx[pp];
+      STMF_IDX(c[u], S.len_other);
       a1[u] = S.t1[pp];
       a2[u] = S.t2[pp];
       a[u] = ok ? (int)S.ag[pp] : -1;  // -1: slot beyond the segment (contributes 0)
@@ -1163,6 +1186,25 @@ __device__ __forceinline__ void pass2_seg(const SideB<T>& S, const typename Vec1
   }
 }
 
+// the second residuation of a line for the kEG evals of a group: per-eval minima of
+// x - v' over the line's entries (pass 1), reduced over the warp; every lane ends with
+// all kEG values
+template <typename T, int VM>
+__device__ __forceinline__ void line_min8(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+                                          const T* __restrict__ base, const T (&s)[kEG], int beg, int sp, int end,
+                                          int lane, T (&mn)[kEG]) {
+#pragma unroll
+  for (int q = 0; q < kEG; q++) mn[q] = tinf<T>();
+  T mn0 = tinf<T>();
+  if (VM == 2 && sp > beg) pass1_seg<T, VM, true>(S, pl, base, s, beg, sp, lane, mn, mn0);
+  pass1_seg<T, VM, false>(S, pl, base, s, sp, end, lane, mn, mn0);
+#pragma unroll
+  for (int q = 0; q < kEG; q++) mn[q] = vmin(mn[q], mn0);
+  T r = warp_reduce8<T, false>(mn, lane);
+#pragma unroll
+  for (int q = 0; q < kEG; q++) mn[q] = __shfl_sync(0xffffffffu, r, q << 2);
+}
+
 // VM: 0 = planar, per-eval k; 1 = planar, one k for the group (Q shared per
 // entry); 2 = one k, F-ULF values recomputed inline (no per-eval gathers), and with
 // a hit partition (S.split) the entries whose column is not given in row i share
@@ -1189,20 +1231,12 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   const int sp = (VM == 2 && S.split) ? S.split[L] : beg;  // [beg, sp): shared values
   T mn[EG];
   if (S.mode == 2) {
-    // sharded F-URF second half: the line values are the all-reduced minima
+    // line values computed before this pass: the sharded F-URF all-reduced minima, or
+    // the statistics walk of k_pass1_fast
 #pragma unroll
     for (int q = 0; q < EG; q++) mn[q] = S.out[(int64_t)(e0 + (q < ne ? q : ne - 1)) * nlines + L];
   } else {
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = tinf<T>();
-    T mn0 = tinf<T>();
-    if (VM == 2 && sp > beg) pass1_seg<T, VM, true>(S, pl, base, s, beg, sp, lane, mn, mn0);
-    pass1_seg<T, VM, false>(S, pl, base, s, sp, end, lane, mn, mn0);
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], mn0);
-    T r = warp_reduce8<T, false>(mn, lane);
-#pragma unroll
-    for (int q = 0; q < EG; q++) mn[q] = __shfl_sync(0xffffffffu, r, q << 2);
+    line_min8<T, VM>(S, pl, base, s, beg, sp, end, lane, mn);
   }
   if (lane < ne) {
     T w = lane_pick<EG>(mn, lane);

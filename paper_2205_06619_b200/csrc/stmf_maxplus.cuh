@@ -232,13 +232,13 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
 // stride RS (U: m x RS, V: n x RS; padding = -inf, so it never wins a max).
 //
 // Per tile (one block of 256 threads, persistent over tiles): the factor rows of the
-// tile are staged in shared memory; then per chunk of 32 rows the mask words are
-// decoded into a list of (row, column) codes in exactly the packed-value order (block
-// scan of the row counts, popc ranks within words), and the threads walk that list:
-// one coalesced value load + RQ float4 loads of each factor row per given entry,
-// FADD2 pairs and 3-input max.  Exact accumulation as the dense kernel.
+// tile are staged in shared memory, the tile's 128 x 4 mask words (prefetched into
+// registers while the previous tile computed) are decoded into a list of (row, column)
+// codes in exactly the packed-value order (warp scans of the row counts, popc ranks
+// within words), and the threads walk that list: one coalesced value load + RQ float4
+// loads of each factor row per given entry, FADD2 pairs and 3-input max.  Exact
+// accumulation as the dense kernel.
 constexpr int kSpT = 128;      // tile edge
-constexpr int kSpRows = 32;    // rows decoded per chunk (list <= 32 * 128 codes)
 __host__ __device__ constexpr int sp_stride(int rq) { return rq % 2 ? 4 * rq : 4 * rq + 4; }
 
 template <int RQ>
@@ -248,19 +248,26 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
                       const float* __restrict__ Vrm, u64* __restrict__ acc, int* __restrict__ flags, int F,
                       double exact_limit) {
   constexpr int RS = sp_stride(RQ);
+  constexpr int WR = kSpT / 8;  // rows per warp
   extern __shared__ __align__(16) unsigned char sp_smem[];
   float* Us = reinterpret_cast<float*>(sp_smem);
   float* Vs = Us + kSpT * RS;
-  uint16_t* list = reinterpret_cast<uint16_t*>(Vs + kSpT * RS);
-  __shared__ int rowcnt[kSpRows], rowoff[kSpRows + 1];
+  __shared__ __align__(16) uint4 Mw[kSpT];
   __shared__ double red[8];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint16_t* list = reinterpret_cast<uint16_t*>(Vs + kSpT * RS) + wid * (WR * kSpT);  // this warp's codes
   const int64_t ntx = n / kSpT, T = (m / kSpT) * ntx;
   const int64_t wpr = n / 32;  // mask words per matrix row
   double part = 0.0;
-  for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
+  // the first tile's mask words (one 16-byte load per row); later tiles' are prefetched
+  // into registers while the previous tile computes
+  uint4 mw = make_uint4(0, 0, 0, 0);
+  int64_t t = blockIdx.x;
+  if (t < T && tid < kSpT)
+    mw = __ldg(reinterpret_cast<const uint4*>(mask + ((t / ntx) * kSpT + tid) * wpr + (t % ntx) * (kSpT / 32)));
+  for (; t < T; t += gridDim.x) {
     const int64_t row0 = (t / ntx) * kSpT, col0 = (t % ntx) * kSpT;
-    // factor rows of the tile (L2-resident across tiles)
+    // factor rows of the tile (L2-resident across tiles) and its mask words
     for (int e = tid; e < kSpT * RQ; e += 256) {
       int rr = e / RQ, q = e - rr * RQ;
       *reinterpret_cast<float4*>(Us + rr * RS + 4 * q) =
@@ -268,77 +275,78 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
       *reinterpret_cast<float4*>(Vs + rr * RS + 4 * q) =
           __ldg(reinterpret_cast<const float4*>(Vrm + (col0 + rr) * RS) + q);
     }
-    int64_t vbase = tile_off[t];
-    for (int c0 = 0; c0 < kSpT; c0 += kSpRows) {
-      // row counts of the chunk: warp w, rows 4w..4w+3; lanes 0..3 hold the 4 words
-      const uint32_t* mrow = mask + (row0 + c0) * wpr + col0 / 32;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        int rl = wid * 4 + q;
-        uint32_t w = lane < 4 ? __ldg(mrow + rl * wpr + lane) : 0u;
-        int c = __popc(w);
-        c += __shfl_xor_sync(0xffffffffu, c, 1);
-        c += __shfl_xor_sync(0xffffffffu, c, 2);
-        if (lane == 0) rowcnt[rl] = c;
-      }
-      __syncthreads();
-      if (wid == 0) {
-        int v = rowcnt[lane], x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        rowoff[lane] = x - v;
-        if (lane == 31) rowoff[kSpRows] = x;
-      }
-      __syncthreads();
-      // decode: lane = column within a word; codes in packed (row-major) order
-      const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        int rl = wid * 4 + q;
-        int pos = rowoff[rl];
-#pragma unroll
-        for (int wi = 0; wi < 4; wi++) {
-          uint32_t w = __ldg(mrow + rl * wpr + wi);
-          if ((w >> lane) & 1u) list[pos + __popc(w & lt)] = (uint16_t)(((c0 + rl) << 7) | (wi * 32 + lane));
-          pos += __popc(w);
-        }
-      }
-      __syncthreads();
-      const int total = rowoff[kSpRows];
-      const float* vc = vals + vbase;
-      for (int e = tid; e < total; e += 256) {
-        float x = __ldg(vc + e);
-        int code = list[e];
-        const float4* ur = reinterpret_cast<const float4*>(Us + (code >> 7) * RS);
-        const float4* vr = reinterpret_cast<const float4*>(Vs + (code & 127) * RS);
-        float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
-#pragma unroll
-        for (int q = 0; q < RQ; q++) {
-          float4 u = ur[q], v = vr[q];
-          float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
-          float2 b = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
-          p0 = max3f(p0, a.x, a.y);
-          p1 = max3f(p1, b.x, b.y);
-        }
-        part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
-      }
-      vbase += total;
-      __syncthreads();
+    if (tid < kSpT) Mw[tid] = mw;
+    __syncthreads();
+    const int64_t tn = t + gridDim.x;  // prefetch the next tile's mask words
+    if (tn < T && tid < kSpT)
+      mw = __ldg(reinterpret_cast<const uint4*>(mask + ((tn / ntx) * kSpT + tid) * wpr + (tn % ntx) * (kSpT / 32)));
+    // warp w owns rows [WR w, WR (w + 1)): its values start after every earlier row's
+    int before = 0;
+    for (int rr = lane; rr < WR * wid; rr += 32) {
+      uint4 a = Mw[rr];
+      before += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    // exclusive scan of the warp's row counts (lanes 0..WR-1)
+    uint4 myw = Mw[WR * wid + (lane < WR ? lane : 0)];
+    int cnt = lane < WR ? __popc(myw.x) + __popc(myw.y) + __popc(myw.z) + __popc(myw.w) : 0, inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    const int roff = inc - cnt;
+    // decode: WR rows x 4 words over the warp (2 pairs per lane), codes in packed order
+#pragma unroll
+    for (int h = 0; h < WR * 4 / 32; h++) {
+      int pr = lane + 32 * h;
+      int rl = pr >> 2, wi = pr & 3;
+      uint4 v4 = Mw[WR * wid + rl];
+      uint32_t wd = wi == 0 ? v4.x : wi == 1 ? v4.y : wi == 2 ? v4.z : v4.w;
+      int pos = __shfl_sync(0xffffffffu, roff, rl);
+      if (wi > 0) pos += __popc(v4.x);
+      if (wi > 1) pos += __popc(v4.y);
+      if (wi > 2) pos += __popc(v4.z);
+      int rowcode = (WR * wid + rl) << 7;
+      while (wd) {
+        int b = __ffs(wd) - 1;
+        wd &= wd - 1;
+        list[pos++] = (uint16_t)(rowcode | (wi * 32 + b));
+      }
+    }
+    __syncwarp();
+    // the warp's given entries: coalesced value loads, RQ float4 loads of each factor row
+    const float* vc = vals + tile_off[t] + before;
+    for (int e = lane; e < total; e += 32) {
+      float x = __ldg(vc + e);
+      int code = list[e];
+      const float4* ur = reinterpret_cast<const float4*>(Us + (code >> 7) * RS);
+      const float4* vr = reinterpret_cast<const float4*>(Vs + (code & 127) * RS);
+      float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
+#pragma unroll
+      for (int q = 0; q < RQ; q++) {
+        float4 u = ur[q], v = vr[q];
+        float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
+        float2 b = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
+        p0 = max3f(p0, a.x, a.y);
+        p1 = max3f(p1, b.x, b.y);
+      }
+      part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
+    }
+    __syncthreads();
   }
   for (int o = 16; o; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
   if (lane == 0) red[wid] = part;
   __syncthreads();
   if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 8; w++) s = __dadd_rn(s, red[w]);
+    double sum = 0.0;
+    for (int w = 0; w < 8; w++) sum = __dadd_rn(sum, red[w]);
     int fl = 0;
-    if (!(s < exact_limit)) fl |= 4;
+    if (!(sum < exact_limit)) fl |= 4;
     u64 hi, lo;
-    fx_from_double(s, F, hi, lo, fl);
+    fx_from_double(sum, F, hi, lo, fl);
     fx_atomic_add(acc, hi, lo);
     if (fl) atomicOr(flags, fl);
   }
@@ -346,7 +354,7 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
 
 template <int RQ>
 constexpr size_t sp_smem_bytes() {
-  return sizeof(float) * 2 * kSpT * sp_stride(RQ) + sizeof(uint16_t) * kSpRows * kSpT;
+  return sizeof(float) * 2 * kSpT * sp_stride(RQ) + sizeof(uint16_t) * kSpT * kSpT;
 }
 
 // data preparation for the sampled layout (not timed): per-tile given counts, then the

@@ -76,6 +76,20 @@ def parse_method(name: str):
     raise ValueError(f"cannot parse method name {name!r}")
 
 
+class _SpecStrategy:
+    """The reference's strategy adapter (strategies.py:317-348) for the host part of the
+    plugin protocol: ``orient`` (transpose / permutation with the fit's RNG).  The sweeps
+    themselves run on the device (stmf_run), so there is no ``sweep`` here."""
+
+    def __init__(self, spec: StrategySpec):
+        self.spec = spec
+        self.name = spec.name
+
+    def orient(self, R: MaskedMatrix, rng):
+        from .engine import _orient
+        return _orient(self.spec, R, rng)
+
+
 def fit(R: MaskedMatrix, rank: int, method, config: RunConfig, device: int | None = None, init=None):
     """Fit R with a method name or StrategySpec (strategies.py:351-357).  ``init``:
     optional warm-start factors (engine.run_fit)."""
