@@ -248,26 +248,27 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
                       const float* __restrict__ Vrm, u64* __restrict__ acc, int* __restrict__ flags, int F,
                       double exact_limit) {
   constexpr int RS = sp_stride(RQ);
-  constexpr int WR = kSpT / 8;  // rows per warp
   extern __shared__ __align__(16) unsigned char sp_smem[];
   float* Us = reinterpret_cast<float*>(sp_smem);
   float* Vs = Us + kSpT * RS;
+  uint16_t* list = reinterpret_cast<uint16_t*>(Vs + kSpT * RS);
   __shared__ __align__(16) uint4 Mw[kSpT];
+  __shared__ int rowoff[kSpT + 1], wsum[4];
   __shared__ double red[8];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  uint16_t* list = reinterpret_cast<uint16_t*>(Vs + kSpT * RS) + wid * (WR * kSpT);  // this warp's codes
-  const int64_t ntx = n / kSpT, T = (m / kSpT) * ntx;
+  // tile indices fit in 32 bits (m, n < 2^31 and 128 x 128 tiles)
+  const int ntx = (int)(n / kSpT), T = (int)((m / kSpT) * ntx);
   const int64_t wpr = n / 32;  // mask words per matrix row
   double part = 0.0;
   // the first tile's mask words (one 16-byte load per row); later tiles' are prefetched
   // into registers while the previous tile computes
   uint4 mw = make_uint4(0, 0, 0, 0);
-  int64_t t = blockIdx.x;
+  int t = blockIdx.x;
   if (t < T && tid < kSpT)
-    mw = __ldg(reinterpret_cast<const uint4*>(mask + ((t / ntx) * kSpT + tid) * wpr + (t % ntx) * (kSpT / 32)));
+    mw = __ldg(reinterpret_cast<const uint4*>(mask + ((int64_t)(t / ntx) * kSpT + tid) * wpr + (t % ntx) * (kSpT / 32)));
   for (; t < T; t += gridDim.x) {
-    const int64_t row0 = (t / ntx) * kSpT, col0 = (t % ntx) * kSpT;
-    // factor rows of the tile (L2-resident across tiles) and its mask words
+    const int64_t row0 = (int64_t)(t / ntx) * kSpT, col0 = (int64_t)(t % ntx) * kSpT;
+    // 1. factor rows of the tile (L2-resident across tiles)
     for (int e = tid; e < kSpT * RQ; e += 256) {
       int rr = e / RQ, q = e - rr * RQ;
       *reinterpret_cast<float4*>(Us + rr * RS + 4 * q) =
@@ -275,51 +276,45 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
       *reinterpret_cast<float4*>(Vs + rr * RS + 4 * q) =
           __ldg(reinterpret_cast<const float4*>(Vrm + (col0 + rr) * RS) + q);
     }
-    if (tid < kSpT) Mw[tid] = mw;
+    // 2. row counts, exclusive scan over the tile's 128 rows (warps 0..3)
+    if (tid < kSpT) {
+      Mw[tid] = mw;
+      int c = __popc(mw.x) + __popc(mw.y) + __popc(mw.z) + __popc(mw.w), x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      rowoff[tid] = x - c;  // within the warp; the warp prefixes are added below
+      if (lane == 31) wsum[wid] = x;
+    }
     __syncthreads();
-    const int64_t tn = t + gridDim.x;  // prefetch the next tile's mask words
+    const int tn = t + gridDim.x;  // prefetch the next tile's mask words (consumed at its step 2)
     if (tn < T && tid < kSpT)
-      mw = __ldg(reinterpret_cast<const uint4*>(mask + ((tn / ntx) * kSpT + tid) * wpr + (tn % ntx) * (kSpT / 32)));
-    // warp w owns rows [WR w, WR (w + 1)): its values start after every earlier row's
-    int before = 0;
-    for (int rr = lane; rr < WR * wid; rr += 32) {
-      uint4 a = Mw[rr];
-      before += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
-    }
+      mw = __ldg(reinterpret_cast<const uint4*>(mask + ((int64_t)(tn / ntx) * kSpT + tid) * wpr + (tn % ntx) * (kSpT / 32)));
+    const int pre0 = wsum[0], pre1 = pre0 + wsum[1], pre2 = pre1 + wsum[2];
+    const int total = pre2 + wsum[3];
+    // 3. decode into (row, column) codes in the packed-value order: 2 (row, word) pairs per thread
 #pragma unroll
-    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-    // exclusive scan of the warp's row counts (lanes 0..WR-1)
-    uint4 myw = Mw[WR * wid + (lane < WR ? lane : 0)];
-    int cnt = lane < WR ? __popc(myw.x) + __popc(myw.y) + __popc(myw.z) + __popc(myw.w) : 0, inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, inc, 31);
-    const int roff = inc - cnt;
-    // decode: WR rows x 4 words over the warp (2 pairs per lane), codes in packed order
-#pragma unroll
-    for (int h = 0; h < WR * 4 / 32; h++) {
-      int pr = lane + 32 * h;
+    for (int h = 0; h < 2; h++) {
+      int pr = tid + 256 * h;
       int rl = pr >> 2, wi = pr & 3;
-      uint4 v4 = Mw[WR * wid + rl];
+      uint4 v4 = Mw[rl];
       uint32_t wd = wi == 0 ? v4.x : wi == 1 ? v4.y : wi == 2 ? v4.z : v4.w;
-      int pos = __shfl_sync(0xffffffffu, roff, rl);
+      int pos = rowoff[rl] + (rl >= 96 ? pre2 : rl >= 64 ? pre1 : rl >= 32 ? pre0 : 0);
       if (wi > 0) pos += __popc(v4.x);
       if (wi > 1) pos += __popc(v4.y);
       if (wi > 2) pos += __popc(v4.z);
-      int rowcode = (WR * wid + rl) << 7;
       while (wd) {
         int b = __ffs(wd) - 1;
         wd &= wd - 1;
-        list[pos++] = (uint16_t)(rowcode | (wi * 32 + b));
+        list[pos++] = (uint16_t)((rl << 7) | (wi * 32 + b));
       }
     }
-    __syncwarp();
-    // the warp's given entries: coalesced value loads, RQ float4 loads of each factor row
-    const float* vc = vals + tile_off[t] + before;
-    for (int e = lane; e < total; e += 32) {
+    __syncthreads();
+    // 4. the given entries: one coalesced value load, RQ float4 loads of each factor row
+    const float* vc = vals + tile_off[t];
+    for (int e = tid; e < total; e += 256) {
       float x = __ldg(vc + e);
       int code = list[e];
       const float4* ur = reinterpret_cast<const float4*>(Us + (code >> 7) * RS);
