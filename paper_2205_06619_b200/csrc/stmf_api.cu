@@ -665,6 +665,7 @@ struct Session : SessionBase {
     if (batch_sched.empty()) {
       // first visit of a row: no depth history yet
       int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
+      if (const char* e = getenv("STMF_B0")) b0 = std::max(1, atoi(e));
       for (int b = b0; b < Emax; b *= 4) batch_sched.push_back(b);
       batch_sched.push_back(Emax);
     }
@@ -1535,9 +1536,10 @@ struct Session : SessionBase {
     // sweeps, so the first batch covers 1.25x the candidates the row consumed on
     // its previous visit, floored by the fixed per-batch cost; then 2x growth
     int first = batch_sched[0];
-    if (!fixed_sched && (int64_t)row_depth.size() == m && row_depth[i] > 0)
-      first = (int)std::max<int64_t>(batch_floor,
-                                     std::min<int64_t>(Emax, (int64_t)(sched_scale * row_depth[i]) + sched_add));
+    double dd = (!fixed_sched && (int64_t)row_depth.size() == m && row_depth[i] > 0) ? (double)row_depth[i]
+                : (!fixed_sched && ema_first ? depth_ema : 0.0);
+    if (dd > 0)
+      first = (int)std::max<int64_t>(batch_floor, std::min<int64_t>(Emax, (int64_t)(sched_scale * dd) + sched_add));
     int next = first;
     while (t0 < nc) {
       int E = (int)std::min<int64_t>(nc - t0, fixed_sched ? batch_sched[std::min(bi, batch_sched.size() - 1)] : next);
@@ -1859,6 +1861,9 @@ struct Session : SessionBase {
     rdepth_on_dev = false;
   }
   double depth_ema = 0;            // running mean of accepting depths
+  // rows without depth history (first sweep, or after set_factors): first batch from the
+  // running mean instead of the fixed first size (STMF_EMA_FIRST)
+  bool ema_first = getenv("STMF_EMA_FIRST") ? atoi(getenv("STMF_EMA_FIRST")) != 0 : false;
   // first batch = scale * previous depth + add; later batches grow by `growth`
   double sched_scale = 1.25, sched_growth = 2.0;
   int sched_add = 2;
@@ -2222,6 +2227,8 @@ struct Session : SessionBase {
       h.sweep = (double)R.cur_sweep;
       h.sched_scale = sched_scale; h.sched_growth = sched_growth; h.sched_add = sched_add;
       h.batch_floor = batch_floor; h.Emax = Emax; h.first0 = batch_sched[0];
+      h.ema_first = ema_first ? 1 : 0;
+      h.depth_ema = depth_ema;
       h.cache_k = -1;
       h.tb0 = 0;
       CK(cudaMemcpyAsync(dctl.p, h_ctl, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
@@ -2235,6 +2242,7 @@ struct Session : SessionBase {
       if (h.error == 3) fail(STMF_ERR_NUMERIC, "exact objective window violated (graph sweep, grid 2^-%d)", F);
       for (long long t = 0; t < h.traj_len; t++) traj_append(R, h_traj_t[t], h_traj_e[t]);
       err = h.err;
+      depth_ema = h.depth_ema;
       R.attempts += h.attempts;
       R.accepts += h.accepts;
       R.visits += h.visits;

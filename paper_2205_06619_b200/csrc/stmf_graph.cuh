@@ -82,8 +82,9 @@ __global__ void k_g_row_begin(DevCtl* c, const int64_t* __restrict__ row_ptr, co
   c->visits++;
   int first = c->first0;
   long long d = row_depth[i];
-  if (d > 0) {
-    long long f = (long long)(c->sched_scale * (double)d) + c->sched_add;
+  double dd = d > 0 ? (double)d : (c->ema_first ? c->depth_ema : 0.0);
+  if (dd > 0) {
+    long long f = (long long)(c->sched_scale * dd) + c->sched_add;
     if (f > c->Emax) f = c->Emax;
     if (f < c->batch_floor) f = c->batch_floor;
     first = (int)f;
@@ -106,6 +107,10 @@ __device__ void g_accept(DevCtl* c, const GBufs<T>& B, int w, int q, int op, dou
                          cudaGraphConditionalHandle h_batch, cudaGraphConditionalHandle h_acc) {
   c->attempts += w + 1;
   B.row_depth[c->i] = c->t0 + w / 2 + 1;
+  {
+    double dep = (double)(c->t0 + w / 2 + 1);
+    c->depth_ema = c->depth_ema > 0 ? 0.9 * c->depth_ema + 0.1 * dep : dep;
+  }
   c->err = value;
   c->accepted = 1;
   c->win_op = op;

@@ -78,6 +78,8 @@ struct DevCtl {
   // schedule (Session::row_visit)
   double sched_scale, sched_growth;
   int sched_add, batch_floor, Emax, first0;
+  int ema_first;         // rows without depth history: first batch from depth_ema
+  double depth_ema;      // running mean of accepting depths (candidates)
 };
 
 // ----------------------------------------------------------------------------
