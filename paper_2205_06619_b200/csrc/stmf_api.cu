@@ -664,7 +664,7 @@ struct Session : SessionBase {
     if (const char* e = getenv("STMF_FLOOR")) batch_floor = std::max(1, atoi(e));
     if (batch_sched.empty()) {
       // first visit of a row: no depth history yet
-      int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
+      int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 120000000 / std::max<int64_t>(N, 1)));
       if (const char* e = getenv("STMF_B0")) b0 = std::max(1, atoi(e));
       for (int b = b0; b < Emax; b *= 4) batch_sched.push_back(b);
       batch_sched.push_back(Emax);
@@ -676,7 +676,9 @@ struct Session : SessionBase {
     // (config 4, N ~ 1e8: faster batch growth, +5% row visits/s in sweep 1; config 3,
     // N ~ 1e7: growth 1.5 is 3-6% faster per sweep; profiles/r01_sched.md)
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.5; }
+    // (round 2, config 3: growth 1.3 instead of 1.5 is 8% faster on a sweep without depth
+    // history and 3-7% on sweeps 1-3 of a fit; profiles/r02_sched_c3.log)
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.3; }
     read_sched_env();
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();

@@ -406,7 +406,7 @@ struct ShardGroup : SessionBase {
     nsm = prop.multiProcessorCount;
     int64_t N = 0;
     for (auto v : nnz) N += v;
-    int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 200000000 / std::max<int64_t>(N, 1)));
+    int b0 = (int)std::max<int64_t>(4, std::min<int64_t>(128, 120000000 / std::max<int64_t>(N, 1)));
     for (int b = b0; b < Emax; b *= 4) batch_sched.push_back(b);
     batch_sched.push_back(Emax);
     off_x = ((size_t)4 * n + 15) / 16 * 16;
@@ -416,7 +416,7 @@ struct ShardGroup : SessionBase {
     rowbuf_bytes = off_ag + (size_t)n;
     batch_floor = (int)std::max<int64_t>(1, std::min<int64_t>(128, 8000000 / std::max<int64_t>(N, 1)));
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.5; }
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.3; }
     if (const char* e = getenv("STMF_SCHED")) sscanf(e, "%lf,%d,%lf", &sched_scale, &sched_add, &sched_growth);
     row_depth.assign(m, 0);
     const T* Xp = X_rows;
