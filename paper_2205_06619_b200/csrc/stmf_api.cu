@@ -2517,7 +2517,14 @@ template <int RQ>
 static void launch_sampled(unsigned grid, cudaStream_t st, int64_t m, int64_t n, const uint32_t* M, const float* vals,
                            const int64_t* off, const float* Urm, const float* Vrm, u64* acc, int* flags, int F,
                            double lim) {
-  k_maxplus_err_sampled<RQ><<<grid, 256, sp_smem_bytes<RQ>(), st>>>(m, n, M, vals, off, Urm, Vrm, acc, flags, F, lim);
+  // STMF_C5_DECODE=list: the code-list decode; default: binary-search decode
+  static const bool list = getenv("STMF_C5_DECODE") && !strcmp(getenv("STMF_C5_DECODE"), "list");
+  if (list)
+    k_maxplus_err_sampled<RQ, false><<<grid, 256, sp_smem_bytes<RQ>(), st>>>(m, n, M, vals, off, Urm, Vrm, acc, flags,
+                                                                             F, lim);
+  else
+    k_maxplus_err_sampled<RQ, true><<<grid, 256, sp_smem_bytes<RQ>(), st>>>(m, n, M, vals, off, Urm, Vrm, acc, flags,
+                                                                            F, lim);
 }
 
 static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint64_t seed, int reps, int flush,
@@ -2635,9 +2642,14 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     const void* kf = rq == 1 ? (const void*)k_maxplus_err_sampled<1> : rq == 2 ? (const void*)k_maxplus_err_sampled<2>
                    : rq == 4 ? (const void*)k_maxplus_err_sampled<4> : rq == 8 ? (const void*)k_maxplus_err_sampled<8>
                    : (const void*)k_maxplus_err_sampled<16>;
+    const void* kfs = rq == 1 ? (const void*)k_maxplus_err_sampled<1, true>
+                    : rq == 2 ? (const void*)k_maxplus_err_sampled<2, true>
+                    : rq == 4 ? (const void*)k_maxplus_err_sampled<4, true>
+                    : rq == 8 ? (const void*)k_maxplus_err_sampled<8, true> : (const void*)k_maxplus_err_sampled<16, true>;
     size_t smem = rq == 1 ? sp_smem_bytes<1>() : rq == 2 ? sp_smem_bytes<2>() : rq == 4 ? sp_smem_bytes<4>()
                 : rq == 8 ? sp_smem_bytes<8>() : sp_smem_bytes<16>();
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(kfs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, smem));
     sgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T, (int64_t)prop.multiProcessorCount * std::max(per_sm, 1)));

@@ -429,9 +429,11 @@ __global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const i
       if (a1 == k || a2 == k) {
         top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
       } else {
-        // k held neither top-2 slot: insert its new value (lowest index on max ties)
+        // k held neither top-2 slot: insert its new value (lowest index on max ties);
+        // most entries keep their caches and are not written back
         if (s > b1 || (s == b1 && k < a1)) { b2 = b1; a2 = a1; b1 = s; a1 = k; }
         else if (s > b2) { b2 = s; a2 = k; }
+        else continue;
       }
     }
     t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;

@@ -241,7 +241,7 @@ k_maxplus_err(int64_t m, int64_t n, int r, const float* __restrict__ X, const ui
 constexpr int kSpT = 128;      // tile edge
 __host__ __device__ constexpr int sp_stride(int rq) { return rq % 2 ? 4 * rq : 4 * rq + 4; }
 
-template <int RQ>
+template <int RQ, bool SEARCH = false>
 __global__ void __launch_bounds__(256)
 k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, const float* __restrict__ vals,
                       const int64_t* __restrict__ tile_off, const float* __restrict__ Urm,
@@ -294,6 +294,45 @@ k_maxplus_err_sampled(int64_t m, int64_t n, const uint32_t* __restrict__ mask, c
       mw = __ldg(reinterpret_cast<const uint4*>(mask + ((int64_t)(tn / ntx) * kSpT + tid) * wpr + (tn % ntx) * (kSpT / 32)));
     const int pre0 = wsum[0], pre1 = pre0 + wsum[1], pre2 = pre1 + wsum[2];
     const int total = pre2 + wsum[3];
+    if (SEARCH) {
+      // SEARCH: every thread locates its entries by binary search over the tile's row
+      // offsets and a select within the row's words (no code list; lanes stay converged)
+      int* rg = reinterpret_cast<int*>(list);  // the code-list space holds the global row offsets
+      if (tid < kSpT) rg[tid] = rowoff[tid] + (tid >= 96 ? pre2 : tid >= 64 ? pre1 : tid >= 32 ? pre0 : 0);
+      __syncthreads();
+      const float* vc = vals + tile_off[t];
+      for (int e = tid; e < total; e += 256) {
+        int lo = 0;
+#pragma unroll
+        for (int step = 64; step; step >>= 1)
+          if (rg[lo + step] <= e) lo += step;
+        int kq = e - rg[lo];
+        uint4 v4 = Mw[lo];
+        int c0 = __popc(v4.x), c1 = __popc(v4.y), c2 = __popc(v4.z);
+        uint32_t wd;
+        int wi;
+        if (kq < c0) { wd = v4.x; wi = 0; }
+        else if (kq < c0 + c1) { wd = v4.y; wi = 1; kq -= c0; }
+        else if (kq < c0 + c1 + c2) { wd = v4.z; wi = 2; kq -= c0 + c1; }
+        else { wd = v4.w; wi = 3; kq -= c0 + c1 + c2; }
+        int b = (int)__fns(wd, 0, kq + 1);
+        float x = __ldg(vc + e);
+        const float4* ur = reinterpret_cast<const float4*>(Us + lo * RS);
+        const float4* vr = reinterpret_cast<const float4*>(Vs + (wi * 32 + b) * RS);
+        float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
+#pragma unroll
+        for (int q = 0; q < RQ; q++) {
+          float4 u = ur[q], v = vr[q];
+          float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
+          float2 c = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
+          p0 = max3f(p0, a.x, a.y);
+          p1 = max3f(p1, c.x, c.y);
+        }
+        part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
+      }
+      __syncthreads();
+      continue;
+    }
     // 3. decode into (row, column) codes in the packed-value order: 2 (row, word) pairs per thread
 #pragma unroll
     for (int h = 0; h < 2; h++) {

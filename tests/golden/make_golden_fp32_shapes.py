@@ -40,7 +40,12 @@ CASES = {
     "c4s": (lambda: gen.config4(m=2048, n=16384, rank=20, blocks=8), 20, 3000),
     # config 4 itself: 32768 x 32768, rank 20 (~107 M given entries)
     "c4": (lambda: gen.config4(), 20, 120),
+    # config 3 late in the fit: the state after sweep 24 of the seeded fit (written by the
+    # device engine, tools/long_fit.py; stored in c3_late_state.npz), then K attempts of sweep
+    # 25 -- rows that are stuck reject every candidate, batches run up to Emax
+    "c3late": (lambda: gen.config3(), 10, 2500),
 }
+LATE_STATE = os.path.join(HERE, "c3_late_state.npz")
 
 
 def sha(a: np.ndarray) -> str:
@@ -48,12 +53,20 @@ def sha(a: np.ndarray) -> str:
 
 
 def prepare(name):
+    """(work matrix, U0, rank, K); for "c3late" U0 is the stored late state's U and its V
+    is returned by late_V()."""
     make, rank, K = CASES[name]
     R = make()
     rng = np.random.default_rng(42)
     work, _ = engine._orient_faststmf(R, rng)
     U0 = engine.acol_means(work, rank, 5, rng).astype(work.dtype)
+    if name == "c3late":
+        U0 = np.load(LATE_STATE)["U"].astype(work.dtype)
     return work, U0, rank, K
+
+
+def late_V(work):
+    return np.load(LATE_STATE)["V"].astype(work.dtype)
 
 
 def run(name):
@@ -61,7 +74,10 @@ def run(name):
     work, U0, rank, K = prepare(name)
     X = work.values
     M = work.mask
-    V0 = np.stack([oracle.residuate_row(X, M, U0[:, k]) for k in range(rank)])
+    if name == "c3late":
+        V0 = late_V(work)
+    else:
+        V0 = np.stack([oracle.residuate_row(X, M, U0[:, k]) for k in range(rank)])
     t1 = time.time()
     r = oracle.fit(X, M, U0, V0, budget_sweeps=1, epsilon=0.0, max_attempts=K)
     dt = time.time() - t1
