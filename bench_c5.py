@@ -44,8 +44,11 @@ def main():
         for r in (int(x) for x in args.ranks.split(",")):
             for d in (float(x) for x in args.density.split(",")):
               for lay in args.layouts.split(","):
+                if lay == "lanes" and r > 16:
+                    continue
                 res = _ext.bench_maxplus(m, m, r, d, seed=7, reps=args.reps, flush_l2=True, layout=lay)
-                line = {"config": f"c5 m=n={m} r={r} density={d}", "layout": res["layout"], "m": m, "n": m,
+                line = {"config": f"c5 m=n={m} r={r} density={d}", "layout": res["layout"], "kernel": res["kernel"],
+                        "m": m, "n": m,
                         "rank": r, "density": d, "algorithmic_bytes": res["bytes"],
                         "avg_ms": res["avg_ms"], "best_ms": res["best_ms"], "given": int(res["given"]),
                         "objective": res["objective"],

@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 SOURCES = ["stmf_api.cu", "stmf_io.cc"]
 HEADERS = ["stmf_kernels.cuh", "stmf_shard.cuh", "stmf_maxplus.cuh", "stmf_graph.cuh", "stmf_strategies.cuh",
-           "stmf_metrics.cuh", "stmf_fast1.cuh"]
+           "stmf_metrics.cuh", "stmf_fast1.cuh", "stmf_maxplus_lanes.cuh"]
 
 STMF_F64, STMF_F32 = 0, 1
 ERR_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "numeric",
@@ -178,21 +178,34 @@ SEL_TD_A, SEL_TD, SEL_TD_B, SEL_SEQ = 0, 1, 2, 3
 def bench_maxplus(m: int, n: int, rank: int, density: float, seed: int = 0, reps: int = 5,
                   flush_l2: bool = True, device: int | None = None, want_data: bool = False, layout: str = "dense"):
     """Config-5 masked max-plus product + error microbench on device-generated data.
-    layout: "dense" (k_maxplus_err), "sampled" (given values only, k_maxplus_err_sampled)
-    or "auto" (sampled at density <= 0.35)."""
-    code = {"dense": 0, "sampled": 1, "auto": -1}[layout]
+    layout: "dense" (k_maxplus_err), "sampled" (given values only: the lane-compacted kernel
+    k_maxplus_err_lanes when n % 1024 == 0 and rank <= 16, else the tile kernel
+    k_maxplus_err_sampled), "lanes" / "tiles" (demand one of the two sampled kernels) or
+    "auto" (sampled at density <= 0.35).  The result's "kernel" names the one that ran."""
+    code = {"dense": 0, "sampled": 1, "auto": -1, "lanes": 2, "tiles": 1}[layout]
+    prev = os.environ.get("STMF_C5_SAMPLED")
+    if layout == "tiles":
+        os.environ["STMF_C5_SAMPLED"] = "tiles"
     out = np.zeros(8, np.float64)
     X = np.empty((m, n), np.float32) if want_data else None
     M = np.empty(m * n // 32, np.uint32) if want_data else None
     U = np.empty((rank, m), np.float32) if want_data else None
     V = np.empty((rank, n), np.float32) if want_data else None
     p = lambda a: None if a is None else _p(a)  # noqa: E731
-    _check(lib().stmf_bench_maxplus_layout(m, n, rank, float(density), int(seed), int(reps), int(flush_l2),
-                                           default_device() if device is None else int(device), code, _p(out),
-                                           p(X), p(M), p(U), p(V)))
+    try:
+        _check(lib().stmf_bench_maxplus_layout(m, n, rank, float(density), int(seed), int(reps), int(flush_l2),
+                                               default_device() if device is None else int(device), code, _p(out),
+                                               p(X), p(M), p(U), p(V)))
+    finally:
+        if layout == "tiles":
+            if prev is None:
+                os.environ.pop("STMF_C5_SAMPLED", None)
+            else:
+                os.environ["STMF_C5_SAMPLED"] = prev
     res = dict(zip(("avg_ms", "best_ms", "objective", "given", "gbs", "gpairs_per_s", "layout", "bytes"),
                    out.tolist()))
-    res["layout"] = "sampled" if res["layout"] == 1 else "dense"
+    res["kernel"] = {0: "k_maxplus_err", 1: "k_maxplus_err_sampled", 2: "k_maxplus_err_lanes"}[int(res["layout"])]
+    res["layout"] = "sampled" if res["layout"] >= 1 else "dense"
     if want_data:
         mask = np.unpackbits(M.view(np.uint8), bitorder="little").reshape(m, n).astype(bool)
         res["data"] = (X, mask, U.T.copy(), V)

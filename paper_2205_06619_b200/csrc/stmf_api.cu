@@ -2498,6 +2498,7 @@ struct Session : SessionBase {
 #include <memory>
 
 #include "stmf_maxplus.cuh"
+#include "stmf_maxplus_lanes.cuh"
 #include "stmf_shard.cuh"
 
 __global__ void k_popcount(int64_t words, const uint32_t* __restrict__ mask, u64* __restrict__ out) {
@@ -2533,8 +2534,16 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   if (m % kMpTR || n % kMpTC) fail(STMF_ERR_INVALID, "m must be a multiple of %d and n of %d", kMpTR, kMpTC);
   if (r < 1) fail(STMF_ERR_INVALID, "rank must be >= 1");
   if (layout < 0) layout = (density <= 0.35 && r <= 64 && m % kSpT == 0 && n % kSpT == 0) ? 1 : 0;
-  if (layout == 1 && (m % kSpT || n % kSpT)) fail(STMF_ERR_INVALID, "sampled layout: m and n must be multiples of %d", kSpT);
-  if (layout == 1 && r > 64) fail(STMF_ERR_INVALID, "sampled layout: rank must be <= 64");
+  if (layout >= 1 && (m % kSpT || n % kSpT)) fail(STMF_ERR_INVALID, "sampled layout: m and n must be multiples of %d", kSpT);
+  if (layout >= 1 && r > 64) fail(STMF_ERR_INVALID, "sampled layout: rank must be <= 64");
+  // the sampled layout has two kernels: lane-compacted chunks (stmf_maxplus_lanes.cuh: n a multiple of
+  // 1024, rank <= 16) and the older 128 x 128 tiles.  layout 1 picks lanes when it applies
+  // (STMF_C5_SAMPLED=tiles forces the tile kernel), layout 2 demands it.
+  const bool lanes_ok = n % kLnSpan == 0 && m % kLnRows == 0 && r <= 16;
+  if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-compacted layout: n must be a multiple of %d and rank <= 16", kLnSpan);
+  bool lanes = layout == 2;
+  if (layout == 1 && lanes_ok && !(getenv("STMF_C5_SAMPLED") && !strcmp(getenv("STMF_C5_SAMPLED"), "tiles"))) lanes = true;
+  if (layout == 2) layout = 1;
   CK(cudaSetDevice(device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
@@ -2621,7 +2630,56 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   while (4 * rq < r) rq *= 2;
   unsigned sgrid = 0;
   u64 given_h = 0;
-  if (layout == 1) {
+  DevBuf<int> lnmax;
+  int ln_cpw_log2 = 0, ln_stages = 2, ln_cap = 4;
+  size_t ln_smem = 0;
+  if (layout == 1 && lanes) {
+    const int RS = 4 * rq;
+    const int64_t nrc = m / kLnRows, nsp = n / kLnSpan, nch = nrc * nsp;
+    tcnt.alloc(nch + 1); toff.alloc(nch + 1); lnmax.alloc(1);
+    CK(cudaMemsetAsync(tcnt.p + nch, 0, sizeof(int64_t), st));
+    CK(cudaMemsetAsync(lnmax.p, 0, sizeof(int), st));
+    k_ln_count<<<gb, 256, 0, st>>>(m, n, M.p, tcnt.p, lnmax.p); LAUNCH_CK();
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt.p, toff.p, nch + 1, st));
+    DevBuf<uint8_t> tmp;
+    tmp.alloc(tb);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, tcnt.p, toff.p, nch + 1, st));
+    int64_t padded = 0;
+    int maxchunk = 0;
+    CK(cudaMemcpyAsync(&padded, toff.p + nch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&maxchunk, lnmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    vals.alloc((size_t)std::max<int64_t>(padded, 4));
+    CK(cudaMemsetAsync(vals.p, 0, vals.n * sizeof(float), st));
+    k_ln_fill<<<gb, 256, 0, st>>>(m, n, M.p, X.p, toff.p, vals.p); LAUNCH_CK();
+    Urm.alloc((size_t)m * RS); Vrm.alloc((size_t)n * RS);
+    k_sp_factor<<<nblk(m * RS, 256), 256, 0, st>>>(m, r, RS, Ut.p, Urm.p); LAUNCH_CK();
+    k_sp_factor<<<nblk(n * RS, 256), 256, 0, st>>>(n, r, RS, V.p, Vrm.p); LAUNCH_CK();
+    // stages: every warp keeps ln_stages chunks of values in flight; a stage holds the largest chunk
+    // (chunks beyond 6 KB of values, i.e. densities above ~0.35, are read straight from global memory)
+    if (const char* e = getenv("STMF_C5_STAGES")) ln_stages = std::min(kLnMaxStages, std::max(1, atoi(e)));
+    ln_cap = std::min(std::max(maxchunk, 4), 1536);
+    const void* kf = rq == 1 ? (const void*)k_maxplus_err_lanes<1> : rq == 2 ? (const void*)k_maxplus_err_lanes<2>
+                                                                            : (const void*)k_maxplus_err_lanes<4>;
+    ln_smem = rq == 1 ? ln_smem_bytes<1>(ln_stages, ln_cap) : rq == 2 ? ln_smem_bytes<2>(ln_stages, ln_cap)
+                                                                      : ln_smem_bytes<4>(ln_stages, ln_cap);
+    CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ln_smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, ln_smem));
+    per_sm = std::max(per_sm, 1);
+    // chunks per warp run: 8 when that still gives every resident warp a run
+    int cpw = 8;
+    if (const char* e = getenv("STMF_C5_CPW")) cpw = std::max(1, atoi(e));
+    while (cpw > 1 && (nrc % cpw || (nrc / cpw) * nsp < (int64_t)prop.multiProcessorCount * per_sm * 8)) cpw /= 2;
+    while ((1 << ln_cpw_log2) < cpw) ln_cpw_log2++;
+    const int64_t nruns = nrc >> ln_cpw_log2;
+    int64_t K = std::max<int64_t>(1, ((int64_t)prop.multiProcessorCount * per_sm) / nsp);
+    K = std::min<int64_t>(K, (nruns + 7) / 8);
+    sgrid = (unsigned)(K * nsp);
+    given_h = 1;
+    CK(cudaStreamSynchronize(st));
+  } else if (layout == 1) {
     int RS = sp_stride(rq);
     int64_t T = (m / kSpT) * (n / kSpT);
     tcnt.alloc(T + 1); toff.alloc(T + 1);
@@ -2662,7 +2720,17 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(u64), st));
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
-    if (layout == 1) {
+    if (layout == 1 && lanes) {
+      if (rq == 1)
+        k_maxplus_err_lanes<1><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
+      else if (rq == 2)
+        k_maxplus_err_lanes<2><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
+      else
+        k_maxplus_err_lanes<4><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
+    } else if (layout == 1) {
       auto L = rq == 1 ? launch_sampled<1> : rq == 2 ? launch_sampled<2> : rq == 4 ? launch_sampled<4>
              : rq == 8 ? launch_sampled<8> : launch_sampled<16>;
       L(sgrid, st, m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F, exact_limit);
@@ -2704,7 +2772,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   out[3] = (double)given;
   out[4] = bytes / (avg * 1e-3) / 1e9;                    // algorithmic GB/s
   out[5] = (double)(layout == 1 ? given : m * n) * r / (avg * 1e-3) / 1e9;  // G computed (entry, k) pairs / s
-  out[6] = layout;
+  out[6] = layout == 1 && lanes ? 2 : layout;
   out[7] = bytes;
 }
 
@@ -2991,7 +3059,7 @@ int stmf_bench_maxplus_layout(int64_t m, int64_t n, int rank, double density, ui
                               int device, int layout, double* out8, float* X_out, uint32_t* mask_out, float* U_out,
                               float* V_out) {
   if (!out8) return set_err(STMF_ERR_INVALID, "null output");
-  if (layout < -1 || layout > 1) return set_err(STMF_ERR_INVALID, "layout must be -1, 0 or 1");
+  if (layout < -1 || layout > 2) return set_err(STMF_ERR_INVALID, "layout must be -1, 0, 1 or 2");
   GUARD(maxplus_bench_impl(m, n, rank, density, seed, reps, flush_l2, device, out8, X_out, mask_out, U_out, V_out,
                            layout));
 }

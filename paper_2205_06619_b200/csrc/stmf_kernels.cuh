@@ -402,41 +402,79 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 }
 
 // flat over the N given entries of one order (rowof/colof: the entry's row and
-// column) -> perfectly balanced whatever the line lengths
+// column) -> perfectly balanced whatever the line lengths.  Each thread takes kProdU
+// entries per iteration and issues all their loads (indices, cached top-2, then the
+// k-term gathers) before any decision: the pass is a streaming update bound by memory
+// latency, so the loads in flight per thread set its rate (round 2: 19% of HBM at
+// config 4 with one entry per thread and iteration).
+#ifndef STMF_PROD_U
+#define STMF_PROD_U 4
+#endif
+constexpr int kProdU = STMF_PROD_U;
 template <typename T>
-__global__ void k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
-                           int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
-                           const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
-                           T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2,
-                           const int* __restrict__ kdev = nullptr) {
+__global__ void __launch_bounds__(256)
+k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
+           int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
+           const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
+           T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2,
+           const int* __restrict__ kdev = nullptr) {
   if (kdev) k = *kdev;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = rowof[p], c = colof[p];
-    STMF_IDX(r, m);
-    STMF_IDX(c, n);
-    T b1, b2;
-    int a1, a2;
-    if (k < 0) {
+  if (k < 0) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+      int64_t r = rowof[p], c = colof[p];
+      STMF_IDX(r, m);
+      STMF_IDX(c, n);
+      T b1, b2;
+      int a1, a2;
       top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
-    } else {
-      // every load of the incremental update issued up front (memory-level
-      // parallelism): the cached top-2, their indices and the new k-term
-      a1 = ag[p];
-      a2 = ag2[p];
-      b1 = t1[p];
-      b2 = t2[p];
-      T s = add_rn(Ut[(int64_t)k * m + r], V[(int64_t)k * n + c]);
-      if (a1 == k || a2 == k) {
-        top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
+      t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
+    }
+    return;
+  }
+  const T* __restrict__ Uk = Ut + (int64_t)k * m;
+  const T* __restrict__ Vk = V + (int64_t)k * n;
+  const int64_t tile = (int64_t)blockDim.x * kProdU;
+  for (int64_t base = blockIdx.x * tile; base < N; base += (int64_t)gridDim.x * tile) {
+    int64_t p[kProdU];
+    int32_t r[kProdU], c[kProdU];
+    int a1[kProdU], a2[kProdU];
+    T b1[kProdU], b2[kProdU], s[kProdU];
+    bool ok[kProdU];
+#pragma unroll
+    for (int u = 0; u < kProdU; u++) {
+      p[u] = base + u * (int64_t)blockDim.x + threadIdx.x;
+      ok[u] = p[u] < N;
+      const int64_t q = ok[u] ? p[u] : 0;
+      r[u] = rowof[q];
+      c[u] = colof[q];
+      a1[u] = ag[q];
+      a2[u] = ag2[q];
+      b1[u] = t1[q];
+      b2[u] = t2[q];
+    }
+#pragma unroll
+    for (int u = 0; u < kProdU; u++) {
+      STMF_IDX(r[u], m);
+      STMF_IDX(c[u], n);
+      s[u] = add_rn(Uk[r[u]], Vk[c[u]]);
+    }
+#pragma unroll
+    for (int u = 0; u < kProdU; u++) {
+      if (!ok[u]) continue;
+      T n1 = b1[u], n2 = b2[u];
+      int x1 = a1[u], x2 = a2[u];
+      if (x1 == k || x2 == k) {
+        // k held a top-2 slot: recompute over all l
+        top2_vec(Urm + (int64_t)r[u] * rp, Vcm + (int64_t)c[u] * rp, rank, n1, n2, x1, x2);
       } else {
         // k held neither top-2 slot: insert its new value (lowest index on max ties);
         // most entries keep their caches and are not written back
-        if (s > b1 || (s == b1 && k < a1)) { b2 = b1; a2 = a1; b1 = s; a1 = k; }
-        else if (s > b2) { b2 = s; a2 = k; }
+        if (s[u] > n1 || (s[u] == n1 && k < x1)) { n2 = n1; x2 = x1; n1 = s[u]; x1 = k; }
+        else if (s[u] > n2) { n2 = s[u]; x2 = k; }
         else continue;
       }
+      t1[p[u]] = n1; t2[p[u]] = n2; ag[p[u]] = (uint8_t)x1; ag2[p[u]] = (uint8_t)x2;
     }
-    t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
   }
 }
 

@@ -20,7 +20,7 @@ from . import _ext
 from .types import (FactorPair, MaskedMatrix, Orientation, Permutation, RunConfig, Trajectory,
                     UpdateOutcome)
 
-__all__ = ["FitSession", "random_acol_init", "acol_means", "run_fit", "f_ulf", "f_urf",
+__all__ = ["FitSession", "FitRun", "random_acol_init", "acol_means", "run_fit", "f_ulf", "f_urf",
            "stmf_baseline"]
 
 
@@ -254,3 +254,10 @@ def stmf_baseline(R: MaskedMatrix, rank: int, config: RunConfig, device: int | N
     """The original element-wise STMF (engine.py:383-385) on the device kernels."""
     from .strategies import BASELINE
     return run_fit(R, rank, BASELINE, config, device=device)
+
+
+def __getattr__(name):  # engine.FitRun, as in the reference's engine module (engine.py:240-310)
+    if name == "FitRun":
+        from .fitrun import FitRun
+        return FitRun
+    raise AttributeError(name)

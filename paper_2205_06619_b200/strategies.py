@@ -10,9 +10,13 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from .engine import run_fit
+from .fitrun import (UpdateCandidate, byelement_sweep, bymatrix_candidates, bymatrix_step, byrow_seq,  # noqa: F401
+                     byrow_sweep, select_k_td, select_k_td_a, select_k_td_b)
 from .types import MaskedMatrix, RunConfig
 
-__all__ = ["StrategySpec", "BASELINE", "FASTSTMF", "parse_method", "fit", "fast_stmf"]
+__all__ = ["StrategySpec", "BASELINE", "FASTSTMF", "parse_method", "fit", "fast_stmf", "UpdateCandidate",
+           "select_k_td", "select_k_td_a", "select_k_td_b", "byrow_sweep", "byrow_seq", "byelement_sweep",
+           "bymatrix_step", "bymatrix_candidates"]
 
 FAMILIES = ("ByRow", "ByElement", "ByMatrix")
 SELECTIONS = ("SEQ", "TD", "TD_A", "TD_B")

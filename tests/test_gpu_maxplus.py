@@ -40,6 +40,25 @@ def test_sampled_layout_matches_dense_and_restatement(m, n, r, d):
     assert b["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
 
 
+@pytest.mark.parametrize("m,n,r,d", [(128, 1024, 4, 0.1), (256, 2048, 13, 0.3), (128, 1024, 16, 1.0),
+                                     (384, 1024, 1, 0.5), (128, 1024, 8, 0.0), (640, 3072, 3, 0.02)])
+@pytest.mark.parametrize("stages,cpw", [(2, 8), (1, 1), (4, 2)])
+def test_lane_compacted_kernel_matches_tiles_dense_and_restatement(m, n, r, d, stages, cpw, monkeypatch):
+    """k_maxplus_err_lanes (4 x 1024 chunks, lane-compacted values, bulk-copy stages) against the
+    dense kernel, the tile kernel and the restatement; density 1.0 makes every chunk larger than
+    a stage (values straight from global memory), 0.0 and 0.02 give empty chunks and lanes."""
+    monkeypatch.setenv("STMF_C5_STAGES", str(stages))
+    monkeypatch.setenv("STMF_C5_CPW", str(cpw))
+    a = _ext.bench_maxplus(m, n, r, d, seed=3 * m + r, reps=1, flush_l2=False, layout="dense")
+    t = _ext.bench_maxplus(m, n, r, d, seed=3 * m + r, reps=1, flush_l2=False, layout="tiles")
+    b = _ext.bench_maxplus(m, n, r, d, seed=3 * m + r, reps=2, flush_l2=False, layout="lanes", want_data=True)
+    assert b["kernel"] == "k_maxplus_err_lanes" and t["kernel"] == "k_maxplus_err_sampled"
+    assert b["given"] == a["given"]
+    assert b["objective"] == a["objective"] == t["objective"]
+    X, M, U, V = b["data"]
+    assert b["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
+
+
 @pytest.mark.parametrize("r", [4, 16, 64])
 @pytest.mark.parametrize("d", [0.1, 0.5, 1.0])
 def test_config5_4096_matches_restatement(r, d):
@@ -49,14 +68,15 @@ def test_config5_4096_matches_restatement(r, d):
     X, M, U, V = res["data"]
     ref = oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
     assert res["objective"] == ref
-    other = "dense" if res["layout"] == "sampled" else "sampled"
-    assert _ext.bench_maxplus(4096, 4096, r, d, seed=5, reps=1, flush_l2=False, layout=other)["objective"] == ref
+    assert res["kernel"] == ("k_maxplus_err" if d > 0.35 else "k_maxplus_err_lanes" if r <= 16 else "k_maxplus_err_sampled")
+    for other in ("dense", "tiles") + (("lanes",) if r <= 16 else ()):
+        assert _ext.bench_maxplus(4096, 4096, r, d, seed=5, reps=1, flush_l2=False, layout=other)["objective"] == ref
 
 
 def test_config5_16384_rank4_matches_restatement():
     res = _ext.bench_maxplus(16384, 16384, 4, 0.1, seed=9, reps=1, flush_l2=False, want_data=True, layout="auto")
     X, M, U, V = res["data"]
-    assert res["layout"] == "sampled"
+    assert res["layout"] == "sampled" and res["kernel"] == "k_maxplus_err_lanes"
     assert res["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
 
 
