@@ -223,11 +223,13 @@ int stmf_bench_product(stmf_session* s, int reps, int flush_l2, double* ms, doub
 int stmf_bench_maxplus(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps,
                        int flush_l2, int device, double* out6, float* X_out, uint32_t* mask_out,
                        float* U_out, float* V_out);
-/* The same with a choice of layout: 0 = dense tiles (above), 1 = sampled: the given
- * values packed per 128 x 128 tile plus the bit mask, only given entries read and
- * computed (m, n multiples of 128, rank <= 64), -1 = automatic (sampled when
- * density <= 0.35).  out8 = out6 + {layout used, algorithmic bytes per launch}; the
- * GB/s of out8[4] counts the layout's own algorithmic bytes (given values only for 1). */
+/* The same with a choice of layout: 0 = dense tiles (above); 1 = sampled: only the given
+ * entries are stored, read and computed (m, n multiples of 128, rank <= 64) — as lane-coded
+ * chunk records (stmf_maxplus_lanes.cuh) when n is a multiple of 1024 and rank <= 16, else as
+ * packed values per 128 x 128 tile plus the bit mask; 2 = the lane-coded kernel or
+ * STMF_ERR_INVALID; -1 = automatic (sampled when density <= 0.35).  out8 = out6 + {kernel
+ * used (0 dense, 1 tiles, 2 lane-coded), algorithmic bytes per launch}; the GB/s of out8[4]
+ * counts the sampled layout's algorithmic bytes m n / 8 + 4 given + factors for 1 and 2. */
 int stmf_bench_maxplus_layout(int64_t m, int64_t n, int rank, double density, uint64_t seed, int reps,
                               int flush_l2, int device, int layout, double* out8, float* X_out,
                               uint32_t* mask_out, float* U_out, float* V_out);

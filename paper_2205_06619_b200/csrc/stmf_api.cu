@@ -2511,7 +2511,8 @@ __global__ void k_popcount(int64_t words, const uint32_t* __restrict__ mask, u64
 
 // config-5 microbench: data generated on the device (seeded counter-based RNG:
 // X, U, V ~ U[-1, 1) on the 2^-23 grid, iid mask with P(given) = density)
-// layout: 0 = dense tiles (k_maxplus_err), 1 = sampled / compacted (k_maxplus_err_sampled),
+// layout: 0 = dense tiles (k_maxplus_err), 1 = sampled / compacted (k_maxplus_err_lanes or
+// k_maxplus_err_sampled), 2 = k_maxplus_err_lanes demanded,
 // -1 = automatic (sampled when density <= 0.35 and r <= 64: fewer bytes and only given
 // entries computed; measured crossover, profiles/r02_c5_sampled.md)
 template <int RQ>
@@ -2539,7 +2540,7 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   // the sampled layout has two kernels: lane-compacted chunks (stmf_maxplus_lanes.cuh: n a multiple of
   // 1024, rank <= 16) and the older 128 x 128 tiles.  layout 1 picks lanes when it applies
   // (STMF_C5_SAMPLED=tiles forces the tile kernel), layout 2 demands it.
-  const bool lanes_ok = n % kLnSpan == 0 && m % kLnRows == 0 && r <= 16;
+  const bool lanes_ok = n % kLnSpan == 0 && m % kLnRows == 0 && r <= 16;  // (m % 128 == 0 is checked above)
   if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-compacted layout: n must be a multiple of %d and rank <= 16", kLnSpan);
   bool lanes = layout == 2;
   if (layout == 1 && lanes_ok && !(getenv("STMF_C5_SAMPLED") && !strcmp(getenv("STMF_C5_SAMPLED"), "tiles"))) lanes = true;
@@ -2631,8 +2632,10 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   unsigned sgrid = 0;
   u64 given_h = 0;
   DevBuf<int> lnmax;
-  int ln_cpw_log2 = 0, ln_stages = 2, ln_cap = 4;
+  DevBuf<uint8_t> lnrecs;
+  int ln_cpw_log2 = 0, ln_stages = 1, ln_cap = 16;
   size_t ln_smem = 0;
+  int64_t ln_bytes = 0;
   if (layout == 1 && lanes) {
     const int RS = 4 * rq;
     const int64_t nrc = m / kLnRows, nsp = n / kLnSpan, nch = nrc * nsp;
@@ -2645,25 +2648,30 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     DevBuf<uint8_t> tmp;
     tmp.alloc(tb);
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, tcnt.p, toff.p, nch + 1, st));
-    int64_t padded = 0;
-    int maxchunk = 0;
-    CK(cudaMemcpyAsync(&padded, toff.p + nch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&maxchunk, lnmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int64_t units = 0;
+    int maxrec = 0;
+    CK(cudaMemcpyAsync(&units, toff.p + nch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&maxrec, lnmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    vals.alloc((size_t)std::max<int64_t>(padded, 4));
-    CK(cudaMemsetAsync(vals.p, 0, vals.n * sizeof(float), st));
-    k_ln_fill<<<gb, 256, 0, st>>>(m, n, M.p, X.p, toff.p, vals.p); LAUNCH_CK();
+    ln_bytes = units * 16;
+    lnrecs.alloc((size_t)std::max<int64_t>(ln_bytes, 16));
+    CK(cudaMemsetAsync(lnrecs.p, 0, lnrecs.n, st));
+    k_ln_fill<<<gb, 256, 0, st>>>(m, n, M.p, X.p, toff.p, lnrecs.p); LAUNCH_CK();
     Urm.alloc((size_t)m * RS); Vrm.alloc((size_t)n * RS);
     k_sp_factor<<<nblk(m * RS, 256), 256, 0, st>>>(m, r, RS, Ut.p, Urm.p); LAUNCH_CK();
     k_sp_factor<<<nblk(n * RS, 256), 256, 0, st>>>(n, r, RS, V.p, Vrm.p); LAUNCH_CK();
-    // stages: every warp keeps ln_stages chunks of values in flight; a stage holds the largest chunk
-    // (chunks beyond 6 KB of values, i.e. densities above ~0.35, are read straight from global memory)
+    // stages: every warp keeps ln_stages records in flight; a stage holds the largest record, as
+    // long as 8 warps x stages fit beside the V span (larger records, i.e. high densities, are read
+    // straight from global memory)
     if (const char* e = getenv("STMF_C5_STAGES")) ln_stages = std::min(kLnMaxStages, std::max(1, atoi(e)));
-    ln_cap = std::min(std::max(maxchunk, 4), 1536);
+    const size_t vbytes = sizeof(float4) * rq * kLnSpan;
+    const size_t budget = (size_t)200 * 1024 - vbytes;
+    ln_cap = std::max(maxrec, 96);
+    while (ln_stages > 1 && (size_t)8 * ln_stages * ln_cap > budget) ln_stages--;
+    if ((size_t)8 * ln_stages * ln_cap > budget) ln_cap = (int)(budget / 8) & ~15;
     const void* kf = rq == 1 ? (const void*)k_maxplus_err_lanes<1> : rq == 2 ? (const void*)k_maxplus_err_lanes<2>
                                                                             : (const void*)k_maxplus_err_lanes<4>;
-    ln_smem = rq == 1 ? ln_smem_bytes<1>(ln_stages, ln_cap) : rq == 2 ? ln_smem_bytes<2>(ln_stages, ln_cap)
-                                                                      : ln_smem_bytes<4>(ln_stages, ln_cap);
+    ln_smem = vbytes + (size_t)8 * ln_stages * ln_cap;
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ln_smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, ln_smem));
@@ -2679,6 +2687,10 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     sgrid = (unsigned)(K * nsp);
     given_h = 1;
     CK(cudaStreamSynchronize(st));
+    if (getenv("STMF_C5_VERBOSE"))
+      fprintf(stderr, "[stmf c5] lane-coded layout: %lld chunks, records %lld bytes (+ %lld of offsets), largest %d, "
+              "stages %d x %d B, cpw %d, grid %u x 256, %d blocks/SM, smem %zu\n", (long long)nch, (long long)ln_bytes,
+              (long long)(nch + 1) * 8, maxrec, ln_stages, ln_cap, cpw, sgrid, per_sm, ln_smem);
   } else if (layout == 1) {
     int RS = sp_stride(rq);
     int64_t T = (m / kSpT) * (n / kSpT);
@@ -2722,13 +2734,13 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaEventRecord(e0, st));
     if (layout == 1 && lanes) {
       if (rq == 1)
-        k_maxplus_err_lanes<1><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<1><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
       else if (rq == 2)
-        k_maxplus_err_lanes<2><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<2><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
       else
-        k_maxplus_err_lanes<4><<<sgrid, 256, ln_smem, st>>>(m, n, M.p, vals.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<4><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
     } else if (layout == 1) {
       auto L = rq == 1 ? launch_sampled<1> : rq == 2 ? launch_sampled<2> : rq == 4 ? launch_sampled<4>

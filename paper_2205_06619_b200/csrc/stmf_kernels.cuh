@@ -408,7 +408,7 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 // latency, so the loads in flight per thread set its rate (round 2: 19% of HBM at
 // config 4 with one entry per thread and iteration).
 #ifndef STMF_PROD_U
-#define STMF_PROD_U 4
+#define STMF_PROD_U 2
 #endif
 constexpr int kProdU = STMF_PROD_U;
 template <typename T>
