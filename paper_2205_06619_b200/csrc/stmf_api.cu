@@ -345,6 +345,8 @@ struct Session : SessionBase {
   // padded to 16 bytes, so an entry's factor rows are contiguous vector loads
   DevBuf<T> Urm, Vcm;
   DevBuf<int32_t> rowof_r, colof_c;  // row of each CSR entry, column of each CSC entry
+  DevBuf<int32_t> prod_list;         // k_product2: entries whose top-2 held the changed index (recomputed densely)
+  DevBuf<int> prod_cnt;              // its length + the reset ticket
   // lines longer than long_thr entries are evaluated block-per-line (k_phaseB_long)
   int64_t long_thr = 4096;
   // phase-B item order: group-major when both orders' entry data fit comfortably in L2
@@ -703,7 +705,7 @@ struct Session : SessionBase {
                             (const void*)k_cand_row<T, 1>, (const void*)k_cand_row<T, 4>,
                             (const void*)k_residuals_delta_multi<T>, (const void*)k_sort_delta_multi<T>,
                             (const void*)k_merge_delta_multi<T>, (const void*)k_pw_leaves8_multi<T>,
-                            (const void*)k_pw_combine_multi_smem<T>, (const void*)k_product2<T>,
+                            (const void*)k_pw_combine_multi_smem<T>, (const void*)k_product2<T>, (const void*)k_product2_slow<T>,
                             (const void*)k_scores<T>, (const void*)k_line_stats<T>, (const void*)k_g_commit<T>,
                             (const void*)k_g_decide<T>, (const void*)k_g_decide_esc<T>, (const void*)k_g_zero,
                             (const void*)k_g_row_begin, (const void*)k_g_row_end, (const void*)k_g_fb_check};
@@ -713,6 +715,8 @@ struct Session : SessionBase {
                               (int)kCombineSmem));
     }
     rowof_r.alloc(N); colof_c.alloc(N);
+    prod_list.alloc(N); prod_cnt.alloc(2);
+    CK(cudaMemsetAsync(prod_cnt.p, 0, 2 * sizeof(int), st));
     k_line_of<<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, rowof_r.p); LAUNCH_CK();
     k_line_of<<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, colof_c.p); LAUNCH_CK();
     // grid of the given data (binary32 mode)
@@ -935,11 +939,11 @@ struct Session : SessionBase {
       // cache_k >= 0: only factor index cache_k changed since the caches were valid
       int kk = cache_k;
       unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
-      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
-                                           t1r.p, t2r.p, agr.p, a2r.p);
+      launch_product2<T>(st, gflat, nsm, N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk, t1r.p,
+                         t2r.p, agr.p, a2r.p, nullptr, prod_list.p, prod_cnt.p);
       LAUNCH_CK();
-      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
-                                           t1c.p, t2c.p, agc.p, a2c.p);
+      launch_product2<T>(st, gflat, nsm, N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk, t1c.p,
+                         t2c.p, agc.p, a2c.p, nullptr, prod_list.p, prod_cnt.p);
       LAUNCH_CK();
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
                                                    !kExact, exact_limit, flags.p);
@@ -2139,8 +2143,8 @@ struct Session : SessionBase {
       k_line_stats<T><<<warps_grid(m), 256, 0, st3>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
                                                          kc, n, m);
       CK(cudaEventRecord(ev_join3, st3));
-      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
-                                           t1r.p, t2r.p, agr.p, a2r.p, kc);
+      launch_product2<T>(st, gflat, nsm, N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0, t1r.p,
+                         t2r.p, agr.p, a2r.p, kc, prod_list.p, prod_cnt.p);
       if (!kExact) {
         // fp64 direct accept: the numpy replica of the committed state (residuals from
         // the new CSR product) on a second branch, overlapped with the remaining caches
@@ -2159,8 +2163,8 @@ struct Session : SessionBase {
         k_g_fb1_check<<<1, 1, 0, st2>>>(c, d_pwout.p, h_fb1);
         CK(cudaEventRecord(ev_join, st2));
       }
-      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
-                                           t1c.p, t2c.p, agc.p, a2c.p, kc);
+      launch_product2<T>(st, gflat, nsm, N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0, t1c.p,
+                         t2c.p, agc.p, a2c.p, kc, prod_list.p, prod_cnt.p);
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
                                                    !kExact, exact_limit, flags.p);
       CK(cudaStreamWaitEvent(st, ev_join3, 0));
@@ -2540,8 +2544,9 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   // the sampled layout has two kernels: lane-compacted chunks (stmf_maxplus_lanes.cuh: n a multiple of
   // 1024, rank <= 16) and the older 128 x 128 tiles.  layout 1 picks lanes when it applies
   // (STMF_C5_SAMPLED=tiles forces the tile kernel), layout 2 demands it.
-  const bool lanes_ok = n % kLnSpan == 0 && m % kLnRows == 0 && r <= 16;  // (m % 128 == 0 is checked above)
-  if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-compacted layout: n must be a multiple of %d and rank <= 16", kLnSpan);
+  const int ln_rq = r <= 4 ? 1 : r <= 8 ? 2 : 4, ln_sp = ln_span(ln_rq);  // (m % 128 == 0 is checked above)
+  const bool lanes_ok = n % ln_sp == 0 && m % kLnRows == 0 && r <= 16;
+  if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-coded layout: n must be a multiple of %d and rank <= 16", ln_sp);
   bool lanes = layout == 2;
   if (layout == 1 && lanes_ok && !(getenv("STMF_C5_SAMPLED") && !strcmp(getenv("STMF_C5_SAMPLED"), "tiles"))) lanes = true;
   if (layout == 2) layout = 1;
@@ -2638,11 +2643,11 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   int64_t ln_bytes = 0;
   if (layout == 1 && lanes) {
     const int RS = 4 * rq;
-    const int64_t nrc = m / kLnRows, nsp = n / kLnSpan, nch = nrc * nsp;
+    const int64_t nrc = m / kLnRows, nsp = n / ln_sp, nch = nrc * nsp;
     tcnt.alloc(nch + 1); toff.alloc(nch + 1); lnmax.alloc(1);
     CK(cudaMemsetAsync(tcnt.p + nch, 0, sizeof(int64_t), st));
     CK(cudaMemsetAsync(lnmax.p, 0, sizeof(int), st));
-    k_ln_count<<<gb, 256, 0, st>>>(m, n, M.p, tcnt.p, lnmax.p); LAUNCH_CK();
+    k_ln_count<<<gb, 256, 0, st>>>(m, n, ln_sp, M.p, tcnt.p, lnmax.p); LAUNCH_CK();
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt.p, toff.p, nch + 1, st));
     DevBuf<uint8_t> tmp;
@@ -2656,40 +2661,40 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     ln_bytes = units * 16;
     lnrecs.alloc((size_t)std::max<int64_t>(ln_bytes, 16));
     CK(cudaMemsetAsync(lnrecs.p, 0, lnrecs.n, st));
-    k_ln_fill<<<gb, 256, 0, st>>>(m, n, M.p, X.p, toff.p, lnrecs.p); LAUNCH_CK();
+    k_ln_fill<<<gb, 256, 0, st>>>(m, n, ln_sp, M.p, X.p, toff.p, lnrecs.p); LAUNCH_CK();
     Urm.alloc((size_t)m * RS); Vrm.alloc((size_t)n * RS);
     k_sp_factor<<<nblk(m * RS, 256), 256, 0, st>>>(m, r, RS, Ut.p, Urm.p); LAUNCH_CK();
     k_sp_factor<<<nblk(n * RS, 256), 256, 0, st>>>(n, r, RS, V.p, Vrm.p); LAUNCH_CK();
-    // stages: every warp keeps ln_stages records in flight; a stage holds the largest record, as
-    // long as 8 warps x stages fit beside the V span (larger records, i.e. high densities, are read
-    // straight from global memory)
+    // one record in flight per warp and stage; a stage holds the largest record as long as two
+    // blocks still fit an SM beside their V spans (larger records, i.e. the densest chunks or high
+    // densities, are read straight from global memory)
     if (const char* e = getenv("STMF_C5_STAGES")) ln_stages = std::min(kLnMaxStages, std::max(1, atoi(e)));
-    const size_t vbytes = sizeof(float4) * rq * kLnSpan;
-    const size_t budget = (size_t)200 * 1024 - vbytes;
-    ln_cap = std::max(maxrec, 96);
-    while (ln_stages > 1 && (size_t)8 * ln_stages * ln_cap > budget) ln_stages--;
-    if ((size_t)8 * ln_stages * ln_cap > budget) ln_cap = (int)(budget / 8) & ~15;
+    const size_t vbytes = sizeof(float4) * rq * ln_sp;
+    const size_t per_block = (size_t)prop.sharedMemPerMultiprocessor / 2 - 3072;  // static + reserved shared memory
+    const size_t budget = per_block > vbytes ? per_block - vbytes : 0;
+    ln_cap = std::max(maxrec, 128);
+    if ((size_t)kLnWarps * ln_stages * ln_cap > budget) ln_cap = std::max<int>(128, (int)(budget / (kLnWarps * ln_stages)) & ~15);
     const void* kf = rq == 1 ? (const void*)k_maxplus_err_lanes<1> : rq == 2 ? (const void*)k_maxplus_err_lanes<2>
                                                                             : (const void*)k_maxplus_err_lanes<4>;
-    ln_smem = vbytes + (size_t)8 * ln_stages * ln_cap;
+    ln_smem = vbytes + (size_t)kLnWarps * ln_stages * ln_cap;
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ln_smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, ln_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 32 * kLnWarps, ln_smem));
     per_sm = std::max(per_sm, 1);
     // chunks per warp run: 8 when that still gives every resident warp a run
     int cpw = 8;
     if (const char* e = getenv("STMF_C5_CPW")) cpw = std::max(1, atoi(e));
-    while (cpw > 1 && (nrc % cpw || (nrc / cpw) * nsp < (int64_t)prop.multiProcessorCount * per_sm * 8)) cpw /= 2;
+    while (cpw > 1 && (nrc % cpw || (nrc / cpw) * nsp < (int64_t)prop.multiProcessorCount * per_sm * kLnWarps)) cpw /= 2;
     while ((1 << ln_cpw_log2) < cpw) ln_cpw_log2++;
     const int64_t nruns = nrc >> ln_cpw_log2;
     int64_t K = std::max<int64_t>(1, ((int64_t)prop.multiProcessorCount * per_sm) / nsp);
-    K = std::min<int64_t>(K, (nruns + 7) / 8);
+    K = std::min<int64_t>(K, (nruns + kLnWarps - 1) / kLnWarps);
     sgrid = (unsigned)(K * nsp);
     given_h = 1;
     CK(cudaStreamSynchronize(st));
     if (getenv("STMF_C5_VERBOSE"))
       fprintf(stderr, "[stmf c5] lane-coded layout: %lld chunks, records %lld bytes (+ %lld of offsets), largest %d, "
-              "stages %d x %d B, cpw %d, grid %u x 256, %d blocks/SM, smem %zu\n", (long long)nch, (long long)ln_bytes,
+              "stages %d x %d B, cpw %d, grid %u x 512, %d blocks/SM, smem %zu\n", (long long)nch, (long long)ln_bytes,
               (long long)(nch + 1) * 8, maxrec, ln_stages, ln_cap, cpw, sgrid, per_sm, ln_smem);
   } else if (layout == 1) {
     int RS = sp_stride(rq);
@@ -2734,13 +2739,13 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaEventRecord(e0, st));
     if (layout == 1 && lanes) {
       if (rq == 1)
-        k_maxplus_err_lanes<1><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<1><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
       else if (rq == 2)
-        k_maxplus_err_lanes<2><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<2><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
       else
-        k_maxplus_err_lanes<4><<<sgrid, 256, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
+        k_maxplus_err_lanes<4><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
                                                             exact_limit, ln_cpw_log2, ln_stages, ln_cap);
     } else if (layout == 1) {
       auto L = rq == 1 ? launch_sampled<1> : rq == 2 ? launch_sampled<2> : rq == 4 ? launch_sampled<4>

@@ -394,6 +394,58 @@ __device__ __forceinline__ void top2_vec(const T* __restrict__ Ur, const T* __re
   }
 }
 
+template <typename T> struct Vec16;  // 16-byte vector of T (defined with the eval layouts below)
+
+// the same with all NV 16-byte vectors of both rows loaded before the first compare: the
+// rows come from L2, and one round of latency instead of NV dependent ones is what the
+// recompute path of k_product2 costs (97% of its warps have a lane on it at rank 20)
+template <typename T, int NV>
+__device__ __forceinline__ void top2_vec_n(const T* __restrict__ Ur, const T* __restrict__ Vc, int rank, T& b1, T& b2,
+                                           int& a1, int& a2) {
+  constexpr int W = 16 / sizeof(T);
+  using V16 = typename Vec16<T>::type;
+  V16 u[NV], v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) {
+    u[i] = __ldg(reinterpret_cast<const V16*>(Ur) + i);
+    v[i] = __ldg(reinterpret_cast<const V16*>(Vc) + i);
+  }
+  b1 = -tinf<T>();
+  b2 = -tinf<T>();
+  a1 = 0;
+  a2 = 255;
+#pragma unroll
+  for (int i = 0; i < NV; i++) {
+    T uu[W], vv[W];
+    Vec16<T>::unpack(u[i], uu, 0);
+    Vec16<T>::unpack(v[i], vv, 0);
+#pragma unroll
+    for (int q = 0; q < W; q++) {
+      int l = i * W + q;
+      if (l >= rank) break;
+      T s = add_rn(uu[q], vv[q]);
+      if (l == 0) { b1 = s; a1 = 0; }
+      else if (s > b1) { b2 = b1; a2 = a1; b1 = s; a1 = l; }
+      else if (s > b2) { b2 = s; a2 = l; }
+    }
+  }
+}
+
+// rp = the padded row length (a multiple of 16 bytes)
+template <typename T>
+__device__ __forceinline__ void top2_rows(const T* __restrict__ Ur, const T* __restrict__ Vc, int rank, int rp, T& b1,
+                                          T& b2, int& a1, int& a2) {
+  switch (rp / (16 / (int)sizeof(T))) {
+    case 1: top2_vec_n<T, 1>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    case 2: top2_vec_n<T, 2>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    case 3: top2_vec_n<T, 3>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    case 4: top2_vec_n<T, 4>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    case 5: top2_vec_n<T, 5>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    case 6: top2_vec_n<T, 6>(Ur, Vc, rank, b1, b2, a1, a2); break;
+    default: top2_vec(Ur, Vc, rank, b1, b2, a1, a2); break;
+  }
+}
+
 // copy factor column k (contiguous in Ut / V rows) into the padded row-major copy
 template <typename T>
 __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict__ src, T* __restrict__ dst) {
@@ -402,22 +454,27 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 }
 
 // flat over the N given entries of one order (rowof/colof: the entry's row and
-// column) -> perfectly balanced whatever the line lengths.  Each thread takes kProdU
-// entries per iteration and issues all their loads (indices, cached top-2, then the
-// k-term gathers) before any decision: the pass is a streaming update bound by memory
-// latency, so the loads in flight per thread set its rate (round 2: 19% of HBM at
-// config 4 with one entry per thread and iteration).
+// column) -> perfectly balanced whatever the line lengths.
+//
+// k < 0: every entry recomputed over all l.  k >= 0 (after an accepted update only factor
+// index k changed): an entry whose top-2 indices exclude k takes the new k-term alone; an
+// entry with k among them needs all l again.  Those are ~2 / rank of the entries, so nearly
+// every warp has one, and recomputing them in place made the whole pass issue-bound on a
+// divergent path that ran with 7-13 of 32 lanes active (ncu at config 4: 8.6-14.6 warp
+// instructions per entry, 19% of HBM; profiles/r02_product2.md).  Instead the pass appends
+// their entry numbers to a list (one atomic per warp) and k_product2_slow recomputes the
+// list with every lane busy.
 #ifndef STMF_PROD_U
 #define STMF_PROD_U 2
 #endif
-constexpr int kProdU = STMF_PROD_U;
+constexpr int kProdU = STMF_PROD_U;  // entries per thread and iteration, their loads issued together
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
            int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
            const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
            T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2,
-           const int* __restrict__ kdev = nullptr) {
+           const int* __restrict__ kdev, int32_t* __restrict__ slow_list, int* __restrict__ slow_cnt) {
   if (kdev) k = *kdev;
   if (k < 0) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
@@ -426,13 +483,15 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
       STMF_IDX(c, n);
       T b1, b2;
       int a1, a2;
-      top2_vec(Urm + r * rp, Vcm + c * rp, rank, b1, b2, a1, a2);
+      top2_rows(Urm + r * rp, Vcm + c * rp, rank, rp, b1, b2, a1, a2);
       t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
     }
     return;
   }
   const T* __restrict__ Uk = Ut + (int64_t)k * m;
   const T* __restrict__ Vk = V + (int64_t)k * n;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int64_t tile = (int64_t)blockDim.x * kProdU;
   for (int64_t base = blockIdx.x * tile; base < N; base += (int64_t)gridDim.x * tile) {
     int64_t p[kProdU];
@@ -460,22 +519,72 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     }
 #pragma unroll
     for (int u = 0; u < kProdU; u++) {
-      if (!ok[u]) continue;
+      // k held a top-2 slot: all l again, by k_product2_slow
+      const bool slow = ok[u] && (a1[u] == k || a2[u] == k);
+      const unsigned bal = __ballot_sync(0xffffffffu, slow);
+      if (bal) {
+        const int leader = __ffs(bal) - 1;
+        int at = 0;
+        if (lane == leader) at = atomicAdd(slow_cnt, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, leader);
+        if (slow) slow_list[at + __popc(bal & lt)] = (int32_t)p[u];
+      }
+      if (!ok[u] || slow) continue;
+      // k held neither top-2 slot: insert its new value (lowest index on max ties);
+      // most entries keep their caches and are not written back
       T n1 = b1[u], n2 = b2[u];
       int x1 = a1[u], x2 = a2[u];
-      if (x1 == k || x2 == k) {
-        // k held a top-2 slot: recompute over all l
-        top2_vec(Urm + (int64_t)r[u] * rp, Vcm + (int64_t)c[u] * rp, rank, n1, n2, x1, x2);
-      } else {
-        // k held neither top-2 slot: insert its new value (lowest index on max ties);
-        // most entries keep their caches and are not written back
-        if (s[u] > n1 || (s[u] == n1 && k < x1)) { n2 = n1; x2 = x1; n1 = s[u]; x1 = k; }
-        else if (s[u] > n2) { n2 = s[u]; x2 = k; }
-        else continue;
-      }
+      if (s[u] > n1 || (s[u] == n1 && k < x1)) { n2 = n1; x2 = x1; n1 = s[u]; x1 = k; }
+      else if (s[u] > n2) { n2 = s[u]; x2 = k; }
+      else continue;
       t1[p[u]] = n1; t2[p[u]] = n2; ag[p[u]] = (uint8_t)x1; ag2[p[u]] = (uint8_t)x2;
     }
   }
+}
+
+// the listed entries recomputed over all l, one entry per lane.  slow_cnt[0] = the list
+// length, slow_cnt[1] = a ticket: the last block to finish resets both, so the pair is ready
+// for the next pass without a memset between kernels (device-resident sweep graphs).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_product2_slow(const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof, int64_t m, int64_t n, int rank,
+                const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, T* __restrict__ t1, T* __restrict__ t2,
+                uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2, const int32_t* __restrict__ slow_list,
+                int* slow_cnt) {
+  const int cnt = *reinterpret_cast<volatile int*>(slow_cnt);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const int64_t p = slow_list[i];
+    const int64_t r = rowof[p], c = colof[p];
+    STMF_IDX(r, m);
+    STMF_IDX(c, n);
+    T b1, b2;
+    int a1, a2;
+    top2_rows(Urm + r * rp, Vcm + c * rp, rank, rp, b1, b2, a1, a2);
+    t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(slow_cnt + 1, 1) == (int)gridDim.x - 1) {
+      slow_cnt[0] = 0;
+      slow_cnt[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// one product pass of one order: the flat update, then the listed recomputes (both launched
+// unconditionally: with k < 0 the list stays empty).  slow_list: N entries, slow_cnt: 2 ints, zero.
+template <typename T>
+inline void launch_product2(cudaStream_t st, unsigned gflat, int nsm, int64_t N, const int32_t* rowof,
+                            const int32_t* colof, int64_t m, int64_t n, int rank, const T* Ut, const T* V,
+                            const T* Urm, const T* Vcm, int rp, int k, T* t1, T* t2, uint8_t* ag, uint8_t* ag2,
+                            const int* kdev, int32_t* slow_list, int* slow_cnt) {
+  k_product2<T><<<gflat, 256, 0, st>>>(N, rowof, colof, m, n, rank, Ut, V, Urm, Vcm, rp, k, t1, t2, ag, ag2, kdev,
+                                       slow_list, slow_cnt);
+  if (k < 0 && !kdev) return;
+  unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)nsm * 8));
+  k_product2_slow<T><<<gs, 256, 0, st>>>(rowof, colof, m, n, rank, Urm, Vcm, rp, t1, t2, ag, ag2, slow_list, slow_cnt);
 }
 
 // line index of every entry of a compacted layout (CSR -> row of each entry)

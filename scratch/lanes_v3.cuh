@@ -18,18 +18,15 @@
 //    shared memory in natural order (16 bytes per column and plane), so the 8 lanes of a
 //    quarter-warp always read 8 different 16-byte bank groups: the per-entry V gather is
 //    conflict free by construction.
-//  * A chunk is one record: [header: 32 u16 lane counts, total, iterations, 32 u8 lane
-//    ranks][u16 slot base per iteration][the values][one byte code per value: (column in
-//    span) >> 3].  Values and codes are stored "iteration-major, compacted": first the first
-//    entry of every lane that has one, then the second of every lane that has two, ...,
-//    within an iteration in order of decreasing lane count (the lane's rank).  Lanes with
-//    more entries rank first, so the lanes active in iteration `it` are exactly ranks
-//    0 .. A_it - 1 and lane l reads slot base[it] + rank[l]: consecutive floats and bytes
-//    across the active lanes (no shared-memory bank conflicts), no padding in memory, and
-//    no ballot / popcount / bit scan in the kernel (the first lane-owned variants spent
-//    their time in exactly those quarter-rate instructions).  The record replaces the bit
-//    mask (the codes carry the positions): 5 bytes per given entry + ~200 per chunk, less
-//    than the mask + values (m n / 8 + 4 given) below 12% density.
+//  * A chunk is one record: [32 x u16 lane counts + total][the values][one byte code per
+//    value: (column in span) >> 3], values and codes "iteration-major, compacted": first
+//    the first entry of every lane that has one (in lane order), then the second of every
+//    lane that has two, ...  In iteration `it` lane l reads slot base_it +
+//    popc(ballot(it < cnt) & lanemask_lt): consecutive lanes read consecutive floats and
+//    bytes (no shared-memory bank conflicts), with no padding in memory.  No bit scans in
+//    the kernel.  The record replaces the bit mask (the codes carry the positions): 5 bytes
+//    per given entry + 80 per chunk, less than the mask + values (m n / 8 + 4 given) below
+//    12% density.
 //  * Records are 16-byte aligned and ordered span-major, row-chunks ascending, so a warp's
 //    run of chunks is one contiguous byte range; each warp streams its records through a
 //    ring of shared-memory stages filled by 1-D bulk async copies (cp.async.bulk ...
@@ -42,9 +39,8 @@
 namespace stmf {
 
 constexpr int kLnRows = 4;       // rows per chunk (one per quarter-warp)
-constexpr int kLnMaxStages = 2;
-constexpr int kLnWarps = 16;     // warps per block (one V span staged per block)
-constexpr int kLnHeader = 112;   // 32 u16 lane counts, total, iterations, 32 u8 lane ranks; padded to 16 bytes
+constexpr int kLnMaxStages = 4;
+constexpr int kLnHeader = 80;    // 32 u16 lane counts + the total, padded to 16 bytes
 // columns per chunk: 8 column classes x 256 (rank <= 4) or x 128 codes
 __host__ __device__ constexpr int ln_span(int rq) { return rq == 1 ? 2048 : 1024; }
 
@@ -56,9 +52,9 @@ __device__ __forceinline__ void ln_mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-// record bytes of a chunk with n given entries in maxc iterations (16-byte multiple)
-__host__ __device__ __forceinline__ int ln_record_bytes(int n, int maxc) {
-  return kLnHeader + ((2 * maxc + 15) & ~15) + 4 * ((n + 3) & ~3) + ((n + 15) & ~15);
+// record bytes of a chunk with n given entries (16-byte multiple)
+__host__ __device__ __forceinline__ int ln_record_bytes(int n) {
+  return kLnHeader + 4 * ((n + 3) & ~3) + ((n + 15) & ~15);
 }
 
 template <bool STAGED, typename V>
@@ -88,22 +84,22 @@ __device__ __forceinline__ float4 ln_lds4(unsigned a) {
 // an entry is j + 8 * code)
 template <int RQ, bool STAGED>
 __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __restrict__ rg, const float4 (&uu)[RQ],
-                                           unsigned vlane, int lane, double part) {
+                                           unsigned vlane, int lane, unsigned ltmask, double part) {
   const int cnt = ln_ld<STAGED, unsigned short>(rs + 2 * lane, rg + 2 * lane);
   const int n = ln_ld<STAGED, unsigned short>(rs + 64, rg + 64);
-  const int maxc = ln_ld<STAGED, unsigned short>(rs + 66, rg + 66);
-  const int rank = ln_ld<STAGED, unsigned char>(rs + 68 + lane, rg + 68 + lane);
-  const int nb = (2 * maxc + 15) & ~15, np4 = 4 * ((n + 3) & ~3);
-  unsigned bs = rs + kLnHeader, xs = rs + kLnHeader + nb + 4 * rank, cs = rs + kLnHeader + nb + np4 + rank;
-  const unsigned char* bg = rg + kLnHeader;
-  const unsigned char* xg = rg + kLnHeader + nb + 4 * rank;
-  const unsigned char* cg = rg + kLnHeader + nb + np4 + rank;
-  asm volatile("" : "+r"(bs), "+r"(xs), "+r"(cs), "+r"(vlane));  // keep the addresses in registers
+  const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+  unsigned xs = rs + kLnHeader, cs = rs + kLnHeader + 4 * ((n + 3) & ~3);
+  const unsigned char* xg = rg + kLnHeader;
+  const unsigned char* cg = rg + kLnHeader + 4 * ((n + 3) & ~3);
+  asm volatile("" : "+r"(xs), "+r"(cs), "+r"(vlane));  // keep the addresses in registers
+  int base = 0;
   for (int it = 0; it < maxc; ++it) {
-    if (it < cnt) {
-      const int base = ln_ld<STAGED, unsigned short>(bs + 2 * it, bg + 2 * it);
-      const float x = ln_ld<STAGED, float>(xs + 4 * base, xg + 4 * base);
-      const unsigned code = ln_ld<STAGED, unsigned char>(cs + base, cg + base);
+    const bool act = it < cnt;
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const int slot = base + __popc(bal & ltmask);
+      const float x = ln_ld<STAGED, float>(xs + 4 * slot, xg + 4 * slot);
+      const unsigned code = ln_ld<STAGED, unsigned char>(cs + slot, cg + slot);
       const unsigned va = vlane + code * 128u;
       float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
 #pragma unroll
@@ -121,16 +117,17 @@ __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __r
       }
       part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
     }
+    base += __popc(bal);
   }
   return part;
 }
 
-// grid = K * (n / SPAN) blocks of 32 kLnWarps threads (block b: span b % nspans); factors row-major
+// grid = K * (n / SPAN) blocks of 256 threads (block b: span b % nspans); factors row-major
 // with stride 4 RQ (padding -inf).  recs = the chunk records, coff[id] = start of record id in
 // 16-byte units (id = span * (m / 4) + row-chunk).  cpw = chunks per warp run (power of two
 // dividing m / 4).
 template <int RQ>
-__global__ void __launch_bounds__(32 * kLnWarps)
+__global__ void __launch_bounds__(256)
 k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs, const int64_t* __restrict__ coff,
                     const float* __restrict__ Urm, const float* __restrict__ Vrm, u64* __restrict__ acc,
                     int* __restrict__ flags, int F, double exact_limit, int cpw_log2, int nstage, int stage_cap) {
@@ -138,16 +135,16 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
   extern __shared__ __align__(128) unsigned char ln_smem[];
   float4* Vs = reinterpret_cast<float4*>(ln_smem);  // [RQ][SPAN]
   unsigned char* stg = ln_smem + sizeof(float4) * RQ * SPAN;
-  __shared__ __align__(8) uint64_t bars[kLnWarps][kLnMaxStages];
-  __shared__ int64_t meta_off[kLnWarps][kLnMaxStages];
-  __shared__ int meta_bytes[kLnWarps][kLnMaxStages];
-  __shared__ double red[kLnWarps];
+  __shared__ __align__(8) uint64_t bars[8][kLnMaxStages];
+  __shared__ int64_t meta_off[8][kLnMaxStages];
+  __shared__ int meta_bytes[8][kLnMaxStages];
+  __shared__ double red[8];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, q = lane >> 3, j = lane & 7;
   const int nspans = (int)(n / SPAN);
   const int cs = (int)(blockIdx.x % nspans), kb = (int)(blockIdx.x / nspans), K = (int)(gridDim.x / nspans);
   const int64_t nrc = m / kLnRows;
   const int cpw = 1 << cpw_log2;
-  for (int c = tid; c < SPAN; c += 32 * kLnWarps) {
+  for (int c = tid; c < SPAN; c += 256) {
     const float4* src = reinterpret_cast<const float4*>(Vrm + ((int64_t)cs * SPAN + c) * (4 * RQ));
 #pragma unroll
     for (int q2 = 0; q2 < RQ; q2++) Vs[q2 * SPAN + c] = __ldg(src + q2);
@@ -162,7 +159,7 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
 
   // this warp's runs: run r covers row-chunks [r cpw, (r + 1) cpw) of span cs
   const int64_t nruns = nrc >> cpw_log2;
-  const int64_t r0 = (int64_t)kb * kLnWarps + wid, rstep = (int64_t)K * kLnWarps;
+  const int64_t r0 = (int64_t)kb * 8 + wid, rstep = (int64_t)K * 8;
   const int64_t nR = r0 < nruns ? (nruns - r0 + rstep - 1) / rstep : 0;
   const int64_t nT = nR << cpw_log2;
   auto chunk_rc = [&](int64_t t) { return ((r0 + (t >> cpw_log2) * rstep) << cpw_log2) + (t & (cpw - 1)); };
@@ -213,6 +210,8 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
     for (int q2 = 0; q2 < RQ; q2++) uuN[q2] = __ldg(ur + q2);
   };
   prefetch(0);
+  unsigned ltmask;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltmask));
   const unsigned vlane = smem_u32(Vs) + j * 16;
   const unsigned stg_s = smem_u32(mystg);
   double part = 0.0;
@@ -227,9 +226,9 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
     if (bytes <= stage_cap) {
       ln_mbar_wait(&bars[wid][s], (phase >> s) & 1u);
       phase ^= 1u << s;
-      part = ln_chunk<RQ, true>(stg_s + s * stage_cap, nullptr, uu, vlane, lane, part);
+      part = ln_chunk<RQ, true>(stg_s + s * stage_cap, nullptr, uu, vlane, lane, ltmask, part);
     } else {  // a record larger than a stage: read straight from global memory
-      part = ln_chunk<RQ, false>(0, recs + meta_off[wid][s] * 16, uu, vlane, lane, part);
+      part = ln_chunk<RQ, false>(0, recs + meta_off[wid][s] * 16, uu, vlane, lane, ltmask, part);
     }
     __syncwarp();
     issue(t + nstage, s);
@@ -241,7 +240,7 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
   __syncthreads();
   if (tid == 0) {
     double sum = 0.0;
-    for (int w = 0; w < kLnWarps; w++) sum = __dadd_rn(sum, red[w]);
+    for (int w = 0; w < 8; w++) sum = __dadd_rn(sum, red[w]);
     int fl = 0;
     if (!(sum < exact_limit)) fl |= 4;
     u64 hi, lo;
@@ -268,10 +267,10 @@ __global__ void k_ln_count(int64_t m, int64_t n, int span, const uint32_t* __res
   for (int64_t id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; id < nch;
        id += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t cs = id / nrc, rc = id - cs * nrc;
-    const int c = ln_lane_count(mask + (rc * kLnRows + q) * wpr + cs * (span / 32), span, j);
-    const int total = __reduce_add_sync(0xffffffffu, c), maxc = __reduce_max_sync(0xffffffffu, c);
+    int c = ln_lane_count(mask + (rc * kLnRows + q) * wpr + cs * (span / 32), span, j);
+    c = __reduce_add_sync(0xffffffffu, c);
     if (lane == 0) {
-      const int bytes = ln_record_bytes(total, maxc);
+      const int bytes = ln_record_bytes(c);
       cnt[id] = bytes / 16;
       atomicMax(maxrec, bytes);
     }
@@ -282,48 +281,37 @@ __global__ void k_ln_fill(int64_t m, int64_t n, int span, const uint32_t* __rest
                           const int64_t* __restrict__ coff, unsigned char* __restrict__ recs) {
   const int lane = threadIdx.x & 31, q = lane >> 3, j = lane & 7;
   const int64_t nrc = m / kLnRows, nch = nrc * (n / span), wpr = n / 32;
+  const unsigned lt = (1u << lane) - 1u;
   for (int64_t id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; id < nch;
        id += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t cs = id / nrc, rc = id - cs * nrc, row = rc * kLnRows + q;
     const uint32_t* mrow = mask + row * wpr + cs * (span / 32);
     const float* xrow = X + row * n + cs * span;
     const int c = ln_lane_count(mrow, span, j);
-    const int total = __reduce_add_sync(0xffffffffu, c), maxc = __reduce_max_sync(0xffffffffu, c);
-    // rank: lanes by decreasing count, ties by lane
-    int rank = 0;
-    for (int l = 0; l < 32; l++) {
-      const int cl = __shfl_sync(0xffffffffu, c, l);
-      rank += (cl > c) || (cl == c && l < lane);
-    }
+    const int total = __reduce_add_sync(0xffffffffu, c);
     unsigned char* rec = recs + coff[id] * 16;
     unsigned short* hdr = reinterpret_cast<unsigned short*>(rec);
     hdr[lane] = (unsigned short)c;
-    if (lane == 0) { hdr[32] = (unsigned short)total; hdr[33] = (unsigned short)maxc; }
-    rec[68 + lane] = (unsigned char)rank;
-    // base[it] = sum over lanes of min(count, it): the slots used by earlier iterations
-    unsigned short* bases = reinterpret_cast<unsigned short*>(rec + kLnHeader);
-    for (int it0 = 0; it0 < maxc; it0 += 32) {
-      const int it = it0 + lane;
-      int b = 0;
-      for (int l = 0; l < 32; l++) b += min(__shfl_sync(0xffffffffu, c, l), it);
-      if (it < maxc) bases[it] = (unsigned short)b;
-    }
-    __syncwarp();
-    const int nb = (2 * maxc + 15) & ~15;
-    float* xv = reinterpret_cast<float*>(rec + kLnHeader + nb);
-    unsigned char* cd = rec + kLnHeader + nb + 4 * ((total + 3) & ~3);
-    // the lane's entries in column order: entry number e goes to slot base[e] + rank
-    int e = 0;
-    for (int w = 0; w < span / 32; w++) {
-      uint32_t cur = mrow[w] & (0x01010101u << j);
-      while (cur) {
+    if (lane == 0) hdr[32] = (unsigned short)total;
+    float* xv = reinterpret_cast<float*>(rec + kLnHeader);
+    unsigned char* cd = rec + kLnHeader + 4 * ((total + 3) & ~3);
+    // the lane's entries in column order; entry number `it` of every lane that has one goes to
+    // the next slots in lane order (the kernel's compacted iteration-major order)
+    int w = 0, base = 0;
+    uint32_t cur = mrow[0] & (0x01010101u << j);
+    for (;;) {
+      while (cur == 0 && w + 1 < span / 32) cur = mrow[++w] & (0x01010101u << j);
+      const bool act = cur != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      if (!bal) break;
+      if (act) {
         const int b = __ffs(cur) - 1;
         cur &= cur - 1;
-        const int col = w * 32 + b, slot = bases[e] + rank;
+        const int col = w * 32 + b, slot = base + __popc(bal & lt);
         xv[slot] = xrow[col];
         cd[slot] = (unsigned char)(col >> 3);
-        e++;
       }
+      base += __popc(bal);
     }
   }
 }

@@ -40,13 +40,13 @@ def test_sampled_layout_matches_dense_and_restatement(m, n, r, d):
     assert b["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
 
 
-@pytest.mark.parametrize("m,n,r,d", [(128, 1024, 4, 0.1), (256, 2048, 13, 0.3), (128, 1024, 16, 1.0),
-                                     (384, 1024, 1, 0.5), (128, 1024, 8, 0.0), (640, 3072, 3, 0.02)])
+@pytest.mark.parametrize("m,n,r,d", [(128, 2048, 4, 0.1), (256, 2048, 13, 0.3), (128, 1024, 16, 1.0),
+                                     (384, 2048, 1, 0.5), (128, 1024, 8, 0.0), (640, 4096, 3, 0.02)])
 @pytest.mark.parametrize("stages,cpw", [(2, 8), (1, 1), (4, 2)])
 def test_lane_compacted_kernel_matches_tiles_dense_and_restatement(m, n, r, d, stages, cpw, monkeypatch):
-    """k_maxplus_err_lanes (4 x 1024 chunks, lane-compacted values, bulk-copy stages) against the
-    dense kernel, the tile kernel and the restatement; density 1.0 makes every chunk larger than
-    a stage (values straight from global memory), 0.0 and 0.02 give empty chunks and lanes."""
+    """k_maxplus_err_lanes (lane-coded chunk records, bulk-copy stages) against the dense kernel,
+    the tile kernel and the restatement; density 1.0 makes every record larger than a stage
+    (read straight from global memory), 0.0 and 0.02 give empty chunks and lanes."""
     monkeypatch.setenv("STMF_C5_STAGES", str(stages))
     monkeypatch.setenv("STMF_C5_CPW", str(cpw))
     a = _ext.bench_maxplus(m, n, r, d, seed=3 * m + r, reps=1, flush_l2=False, layout="dense")
