@@ -345,8 +345,6 @@ struct Session : SessionBase {
   // padded to 16 bytes, so an entry's factor rows are contiguous vector loads
   DevBuf<T> Urm, Vcm;
   DevBuf<int32_t> rowof_r, colof_c;  // row of each CSR entry, column of each CSC entry
-  DevBuf<int32_t> prod_list;         // k_product2: entries whose top-2 held the changed index (recomputed densely)
-  DevBuf<int> prod_cnt;              // its length + the reset ticket
   // lines longer than long_thr entries are evaluated block-per-line (k_phaseB_long)
   int64_t long_thr = 4096;
   // phase-B item order: group-major when both orders' entry data fit comfortably in L2
@@ -705,7 +703,7 @@ struct Session : SessionBase {
                             (const void*)k_cand_row<T, 1>, (const void*)k_cand_row<T, 4>,
                             (const void*)k_residuals_delta_multi<T>, (const void*)k_sort_delta_multi<T>,
                             (const void*)k_merge_delta_multi<T>, (const void*)k_pw_leaves8_multi<T>,
-                            (const void*)k_pw_combine_multi_smem<T>, (const void*)k_product2<T>, (const void*)k_product2_slow<T>,
+                            (const void*)k_pw_combine_multi_smem<T>, (const void*)k_product2<T>,
                             (const void*)k_scores<T>, (const void*)k_line_stats<T>, (const void*)k_g_commit<T>,
                             (const void*)k_g_decide<T>, (const void*)k_g_decide_esc<T>, (const void*)k_g_zero,
                             (const void*)k_g_row_begin, (const void*)k_g_row_end, (const void*)k_g_fb_check};
@@ -715,8 +713,6 @@ struct Session : SessionBase {
                               (int)kCombineSmem));
     }
     rowof_r.alloc(N); colof_c.alloc(N);
-    prod_list.alloc(N); prod_cnt.alloc(2);
-    CK(cudaMemsetAsync(prod_cnt.p, 0, 2 * sizeof(int), st));
     k_line_of<<<warps_grid(m), 256, 0, st>>>(m, row_ptr.p, rowof_r.p); LAUNCH_CK();
     k_line_of<<<warps_grid(n), 256, 0, st>>>(n, col_ptr.p, colof_c.p); LAUNCH_CK();
     // grid of the given data (binary32 mode)
@@ -939,11 +935,11 @@ struct Session : SessionBase {
       // cache_k >= 0: only factor index cache_k changed since the caches were valid
       int kk = cache_k;
       unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(N, 256), (int64_t)nsm * 16));
-      launch_product2<T>(st, gflat, nsm, N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk, t1r.p,
-                         t2r.p, agr.p, a2r.p, nullptr, prod_list.p, prod_cnt.p);
+      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
+                                           t1r.p, t2r.p, agr.p, a2r.p);
       LAUNCH_CK();
-      launch_product2<T>(st, gflat, nsm, N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk, t1c.p,
-                         t2c.p, agc.p, a2c.p, nullptr, prod_list.p, prod_cnt.p);
+      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, kk,
+                                           t1c.p, t2c.p, agc.p, a2c.p);
       LAUNCH_CK();
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
                                                    !kExact, exact_limit, flags.p);
@@ -2143,8 +2139,8 @@ struct Session : SessionBase {
       k_line_stats<T><<<warps_grid(m), 256, 0, st3>>>(m, row_ptr.p, col_idx.p, xr.p, V.p, rm1.p, rm2.p, rmarg.p, 0,
                                                          kc, n, m);
       CK(cudaEventRecord(ev_join3, st3));
-      launch_product2<T>(st, gflat, nsm, N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0, t1r.p,
-                         t2r.p, agr.p, a2r.p, kc, prod_list.p, prod_cnt.p);
+      k_product2<T><<<gflat, 256, 0, st>>>(N, rowof_r.p, col_idx.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
+                                           t1r.p, t2r.p, agr.p, a2r.p, kc);
       if (!kExact) {
         // fp64 direct accept: the numpy replica of the committed state (residuals from
         // the new CSR product) on a second branch, overlapped with the remaining caches
@@ -2163,8 +2159,8 @@ struct Session : SessionBase {
         k_g_fb1_check<<<1, 1, 0, st2>>>(c, d_pwout.p, h_fb1);
         CK(cudaEventRecord(ev_join, st2));
       }
-      launch_product2<T>(st, gflat, nsm, N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0, t1c.p,
-                         t2c.p, agc.p, a2c.p, kc, prod_list.p, prod_cnt.p);
+      k_product2<T><<<gflat, 256, 0, st>>>(N, row_idx.p, colof_c.p, m, n, rank, Ut.p, V.p, Urm.p, Vcm.p, rp, 0,
+                                           t1c.p, t2c.p, agc.p, a2c.p, kc);
       k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, col_ptr.p, xc.p, t1c.p, agc.p, score.p, colhist.p,
                                                    !kExact, exact_limit, flags.p);
       CK(cudaStreamWaitEvent(st, ev_join3, 0));

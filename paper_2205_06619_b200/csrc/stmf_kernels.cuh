@@ -461,9 +461,11 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 // entry with k among them needs all l again.  Those are ~2 / rank of the entries, so nearly
 // every warp has one, and recomputing them in place made the whole pass issue-bound on a
 // divergent path that ran with 7-13 of 32 lanes active (ncu at config 4: 8.6-14.6 warp
-// instructions per entry, 19% of HBM; profiles/r02_product2.md).  Instead the pass appends
-// their entry numbers to a list (one atomic per warp) and k_product2_slow recomputes the
-// list with every lane busy.
+// instructions per entry, 19% of HBM; profiles/r02_product2.md).  Instead each block
+// collects the entries of its tile that need the recompute in shared memory and its first
+// threads then recompute them one per lane, every lane busy.  (A global list + a second
+// kernel was tried first: the single-address atomics and the scattered second pass made
+// it slower than the divergent version.)
 #ifndef STMF_PROD_U
 #define STMF_PROD_U 2
 #endif
@@ -474,7 +476,7 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
            int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
            const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
            T* __restrict__ t2, uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2,
-           const int* __restrict__ kdev, int32_t* __restrict__ slow_list, int* __restrict__ slow_cnt) {
+           const int* __restrict__ kdev = nullptr) {
   if (kdev) k = *kdev;
   if (k < 0) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
@@ -488,12 +490,16 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     }
     return;
   }
+  __shared__ int s_n;
+  __shared__ int32_t s_p[256 * kProdU];  // the tile's entries that need all l (N < 2^31 per device)
   const T* __restrict__ Uk = Ut + (int64_t)k * m;
   const T* __restrict__ Vk = V + (int64_t)k * n;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t tile = (int64_t)blockDim.x * kProdU;
   for (int64_t base = blockIdx.x * tile; base < N; base += (int64_t)gridDim.x * tile) {
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
     int64_t p[kProdU];
     int32_t r[kProdU], c[kProdU];
     int a1[kProdU], a2[kProdU];
@@ -519,15 +525,15 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     }
 #pragma unroll
     for (int u = 0; u < kProdU; u++) {
-      // k held a top-2 slot: all l again, by k_product2_slow
+      // k held a top-2 slot: all l again, after the tile's flat part
       const bool slow = ok[u] && (a1[u] == k || a2[u] == k);
       const unsigned bal = __ballot_sync(0xffffffffu, slow);
       if (bal) {
         const int leader = __ffs(bal) - 1;
         int at = 0;
-        if (lane == leader) at = atomicAdd(slow_cnt, __popc(bal));
+        if (lane == leader) at = atomicAdd(&s_n, __popc(bal));
         at = __shfl_sync(0xffffffffu, at, leader);
-        if (slow) slow_list[at + __popc(bal & lt)] = (int32_t)p[u];
+        if (slow) s_p[at + __popc(bal & lt)] = (int32_t)p[u];
       }
       if (!ok[u] || slow) continue;
       // k held neither top-2 slot: insert its new value (lowest index on max ties);
@@ -539,52 +545,18 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
       else continue;
       t1[p[u]] = n1; t2[p[u]] = n2; ag[p[u]] = (uint8_t)x1; ag2[p[u]] = (uint8_t)x2;
     }
-  }
-}
-
-// the listed entries recomputed over all l, one entry per lane.  slow_cnt[0] = the list
-// length, slow_cnt[1] = a ticket: the last block to finish resets both, so the pair is ready
-// for the next pass without a memset between kernels (device-resident sweep graphs).
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_product2_slow(const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof, int64_t m, int64_t n, int rank,
-                const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, T* __restrict__ t1, T* __restrict__ t2,
-                uint8_t* __restrict__ ag, uint8_t* __restrict__ ag2, const int32_t* __restrict__ slow_list,
-                int* slow_cnt) {
-  const int cnt = *reinterpret_cast<volatile int*>(slow_cnt);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int64_t p = slow_list[i];
-    const int64_t r = rowof[p], c = colof[p];
-    STMF_IDX(r, m);
-    STMF_IDX(c, n);
-    T b1, b2;
-    int a1, a2;
-    top2_rows(Urm + r * rp, Vcm + c * rp, rank, rp, b1, b2, a1, a2);
-    t1[p] = b1; t2[p] = b2; ag[p] = (uint8_t)a1; ag2[p] = (uint8_t)a2;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(slow_cnt + 1, 1) == (int)gridDim.x - 1) {
-      slow_cnt[0] = 0;
-      slow_cnt[1] = 0;
-      __threadfence();
+    __syncthreads();
+    const int ns = s_n;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+      const int64_t q = s_p[i];
+      const int64_t rr = rowof[q], cc = colof[q];
+      T n1, n2;
+      int x1, x2;
+      top2_rows(Urm + rr * rp, Vcm + cc * rp, rank, rp, n1, n2, x1, x2);
+      t1[q] = n1; t2[q] = n2; ag[q] = (uint8_t)x1; ag2[q] = (uint8_t)x2;
     }
+    __syncthreads();  // s_n and s_p are reused by the next tile
   }
-}
-
-// one product pass of one order: the flat update, then the listed recomputes (both launched
-// unconditionally: with k < 0 the list stays empty).  slow_list: N entries, slow_cnt: 2 ints, zero.
-template <typename T>
-inline void launch_product2(cudaStream_t st, unsigned gflat, int nsm, int64_t N, const int32_t* rowof,
-                            const int32_t* colof, int64_t m, int64_t n, int rank, const T* Ut, const T* V,
-                            const T* Urm, const T* Vcm, int rp, int k, T* t1, T* t2, uint8_t* ag, uint8_t* ag2,
-                            const int* kdev, int32_t* slow_list, int* slow_cnt) {
-  k_product2<T><<<gflat, 256, 0, st>>>(N, rowof, colof, m, n, rank, Ut, V, Urm, Vcm, rp, k, t1, t2, ag, ag2, kdev,
-                                       slow_list, slow_cnt);
-  if (k < 0 && !kdev) return;
-  unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, (int64_t)nsm * 8));
-  k_product2_slow<T><<<gs, 256, 0, st>>>(rowof, colof, m, n, rank, Urm, Vcm, rp, t1, t2, ag, ag2, slow_list, slow_cnt);
 }
 
 // line index of every entry of a compacted layout (CSR -> row of each entry)

@@ -61,21 +61,36 @@ __host__ __device__ __forceinline__ int ln_record_bytes(int n, int maxc) {
   return kLnHeader + ((2 * maxc + 15) & ~15) + 4 * ((n + 3) & ~3) + ((n + 15) & ~15);
 }
 
-template <bool STAGED, typename V>
-__device__ __forceinline__ V ln_ld(unsigned sa, const unsigned char* ga) {
-  V v;
-  if constexpr (STAGED) {
-    if constexpr (sizeof(V) == 4) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(*reinterpret_cast<unsigned*>(&v)) : "r"(sa));
-    else if constexpr (sizeof(V) == 2) asm volatile("ld.shared.u16 %0, [%1];" : "=h"(*reinterpret_cast<unsigned short*>(&v)) : "r"(sa));
-    else {
-      unsigned t;
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(t) : "r"(sa));
-      v = (V)t;
-    }
-  } else {
-    v = __ldg(reinterpret_cast<const V*>(ga));
-  }
-  return v;
+// small loads from the record: shared memory by 32-bit shared address (STAGED) or global.
+// The narrow ones return the zero-extended value in a 32-bit register (no re-masking).
+template <bool STAGED>
+__device__ __forceinline__ unsigned ln_ld_u8(unsigned sa, const unsigned char* ga) {
+  unsigned t;
+  if constexpr (STAGED) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(t) : "r"(sa));
+  else asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(t) : "l"(ga));
+  return t;
+}
+template <bool STAGED>
+__device__ __forceinline__ unsigned ln_ld_u16(unsigned sa, const unsigned char* ga) {
+  unsigned t;
+  if constexpr (STAGED) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(t) : "r"(sa));
+  else asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(t) : "l"(ga));
+  return t;
+}
+template <bool STAGED>
+__device__ __forceinline__ float ln_ld_f32(unsigned sa, const unsigned char* ga) {
+  float t;
+  if constexpr (STAGED) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(sa));
+  else asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(t) : "l"(ga));
+  return t;
+}
+// four consecutive u16 (8-byte aligned)
+template <bool STAGED>
+__device__ __forceinline__ uint2 ln_ld_b64(unsigned sa, const unsigned char* ga) {
+  uint2 t;
+  if constexpr (STAGED) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(sa));
+  else asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(ga));
+  return t;
 }
 __device__ __forceinline__ float4 ln_lds4(unsigned a) {
   float4 v;
@@ -87,40 +102,50 @@ __device__ __forceinline__ float4 ln_lds4(unsigned a) {
 // lane's U row; vlane = shared address of V column j = lane & 7 of the span (the column of
 // an entry is j + 8 * code)
 template <int RQ, bool STAGED>
+__device__ __forceinline__ double ln_entry(unsigned xs, unsigned cs, const unsigned char* __restrict__ xg,
+                                           const unsigned char* __restrict__ cg, unsigned base,
+                                           const float4 (&uu)[RQ], unsigned vlane, double part) {
+  const float x = ln_ld_f32<STAGED>(xs + 4 * base, xg + 4 * base);
+  const unsigned code = ln_ld_u8<STAGED>(cs + base, cg + base);
+  const unsigned va = vlane + code * 128u;
+  float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
+#pragma unroll
+  for (int q = 0; q < RQ; q++) {
+    const float4 v = ln_lds4(va + q * (ln_span(RQ) * 16)), u = uu[q];
+    const float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
+    const float2 c = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
+    if (q == 0) {
+      p0 = fmaxf(a.x, a.y);
+      p1 = fmaxf(c.x, c.y);
+    } else {
+      p0 = max3f(p0, a.x, a.y);
+      p1 = max3f(p1, c.x, c.y);
+    }
+  }
+  return __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
+}
+
+template <int RQ, bool STAGED>
 __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __restrict__ rg, const float4 (&uu)[RQ],
                                            unsigned vlane, int lane, double part) {
-  const int cnt = ln_ld<STAGED, unsigned short>(rs + 2 * lane, rg + 2 * lane);
-  const int n = ln_ld<STAGED, unsigned short>(rs + 64, rg + 64);
-  const int maxc = ln_ld<STAGED, unsigned short>(rs + 66, rg + 66);
-  const int rank = ln_ld<STAGED, unsigned char>(rs + 68 + lane, rg + 68 + lane);
+  const int cnt = (int)ln_ld_u16<STAGED>(rs + 2 * lane, rg + 2 * lane);
+  const int n = (int)ln_ld_u16<STAGED>(rs + 64, rg + 64);
+  const int maxc = (int)ln_ld_u16<STAGED>(rs + 66, rg + 66);
+  const unsigned rank = ln_ld_u8<STAGED>(rs + 68 + lane, rg + 68 + lane);
   const int nb = (2 * maxc + 15) & ~15, np4 = 4 * ((n + 3) & ~3);
   unsigned bs = rs + kLnHeader, xs = rs + kLnHeader + nb + 4 * rank, cs = rs + kLnHeader + nb + np4 + rank;
   const unsigned char* bg = rg + kLnHeader;
   const unsigned char* xg = rg + kLnHeader + nb + 4 * rank;
   const unsigned char* cg = rg + kLnHeader + nb + np4 + rank;
   asm volatile("" : "+r"(bs), "+r"(xs), "+r"(cs), "+r"(vlane));  // keep the addresses in registers
-  for (int it = 0; it < maxc; ++it) {
-    if (it < cnt) {
-      const int base = ln_ld<STAGED, unsigned short>(bs + 2 * it, bg + 2 * it);
-      const float x = ln_ld<STAGED, float>(xs + 4 * base, xg + 4 * base);
-      const unsigned code = ln_ld<STAGED, unsigned char>(cs + base, cg + base);
-      const unsigned va = vlane + code * 128u;
-      float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
-#pragma unroll
-      for (int q = 0; q < RQ; q++) {
-        const float4 v = ln_lds4(va + q * (ln_span(RQ) * 16)), u = uu[q];
-        const float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
-        const float2 c = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
-        if (q == 0) {
-          p0 = fmaxf(a.x, a.y);
-          p1 = fmaxf(c.x, c.y);
-        } else {
-          p0 = max3f(p0, a.x, a.y);
-          p1 = max3f(p1, c.x, c.y);
-        }
-      }
-      part = __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
-    }
+  // four iterations per step: their slot bases are one 8-byte load (the base array is padded to
+  // 16 bytes, so the load stays inside the record)
+  for (int it = 0; it < maxc; it += 4) {
+    const uint2 b4 = ln_ld_b64<STAGED>(bs + 2 * it, bg + 2 * it);
+    if (it < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.x & 0xffffu, uu, vlane, part);
+    if (it + 1 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.x >> 16, uu, vlane, part);
+    if (it + 2 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.y & 0xffffu, uu, vlane, part);
+    if (it + 3 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.y >> 16, uu, vlane, part);
   }
   return part;
 }
@@ -130,7 +155,7 @@ __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __r
 // 16-byte units (id = span * (m / 4) + row-chunk).  cpw = chunks per warp run (power of two
 // dividing m / 4).
 template <int RQ>
-__global__ void __launch_bounds__(32 * kLnWarps)
+__global__ void __launch_bounds__(32 * kLnWarps, RQ <= 2 ? 2 : 1)
 k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs, const int64_t* __restrict__ coff,
                     const float* __restrict__ Urm, const float* __restrict__ Vrm, u64* __restrict__ acc,
                     int* __restrict__ flags, int F, double exact_limit, int cpw_log2, int nstage, int stage_cap) {

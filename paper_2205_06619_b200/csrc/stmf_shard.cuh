@@ -295,8 +295,7 @@ struct Shard {
   DevBuf<T> t1r, t2r, t1c, t2c;
   DevBuf<uint8_t> agr, agc, a2r, a2c;
   DevBuf<T> Urm, Vcm;  // row-major factor copies (ml x rp, n x rp) for the product passes
-  DevBuf<int32_t> rowof_r, colof_c, prod_list;
-  DevBuf<int> prod_cnt;
+  DevBuf<int32_t> rowof_r, colof_c;
   DevBuf<int32_t> long_rows, long_cols;  // lines evaluated block-per-line
   int n_long_rows = 0, n_long_cols = 0;
   DevBuf<double> score;
@@ -494,8 +493,6 @@ struct ShardGroup : SessionBase {
       if (!lc.empty()) CK(cudaMemcpy(s.long_cols.p, lc.data(), 4 * lc.size(), cudaMemcpyHostToDevice));
     }
     s.rowof_r.alloc(Nl); s.colof_c.alloc(Nl);
-    s.prod_list.alloc(std::max<int64_t>(Nl, 1)); s.prod_cnt.alloc(2);
-    CK(cudaMemsetAsync(s.prod_cnt.p, 0, 2 * sizeof(int), st));
     k_line_of<<<warps_grid(ml), 256, 0, st>>>(ml, s.row_ptr.p, s.rowof_r.p);
     LAUNCH_CK();
     k_line_of<<<warps_grid(n), 256, 0, st>>>(n, s.col_ptr.p, s.colof_c.p);
@@ -621,13 +618,11 @@ struct ShardGroup : SessionBase {
         Shard<T>& s = *sp;
         CK(cudaMemsetAsync(s.flags.p, 0, sizeof(int), st));
         unsigned gflat = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(s.Nl, 256), (int64_t)nsm * 16));
-        launch_product2<T>(st, gflat, nsm, s.Nl, s.rowof_r.p, s.col_idx.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
-                           s.Vcm.p, rp, cache_k, s.t1r.p, s.t2r.p, s.agr.p, s.a2r.p, nullptr, s.prod_list.p,
-                           s.prod_cnt.p);
+        k_product2<T><<<gflat, 256, 0, st>>>(s.Nl, s.rowof_r.p, s.col_idx.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
+                                             s.Vcm.p, rp, cache_k, s.t1r.p, s.t2r.p, s.agr.p, s.a2r.p);
         LAUNCH_CK();
-        launch_product2<T>(st, gflat, nsm, s.Nl, s.row_idx.p, s.colof_c.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
-                           s.Vcm.p, rp, cache_k, s.t1c.p, s.t2c.p, s.agc.p, s.a2c.p, nullptr, s.prod_list.p,
-                           s.prod_cnt.p);
+        k_product2<T><<<gflat, 256, 0, st>>>(s.Nl, s.row_idx.p, s.colof_c.p, s.ml, n, rank, s.Ut.p, s.V.p, s.Urm.p,
+                                             s.Vcm.p, rp, cache_k, s.t1c.p, s.t2c.p, s.agc.p, s.a2c.p);
         LAUNCH_CK();
         k_scores<T><<<warps_grid(n), 256, 0, st>>>(n, rank, s.col_ptr.p, s.xc.p, s.t1c.p, s.agc.p, s.score.p,
                                                      s.colhist.p, false, exact_limit, s.flags.p);

@@ -44,8 +44,14 @@ CASES = {
     # device engine, tools/long_fit.py; stored in c3_late_state.npz), then K attempts of sweep
     # 25 -- rows that are stuck reject every candidate, batches run up to Emax
     "c3late": (lambda: gen.config3(), 10, 2500),
+    # config 3 at the end of its fit: the state after sweep 41, where the device fit reached its
+    # fixpoint (profiles/r02_c3_fit.md; stored in c3_fixpoint_state.npz).  The first row visit
+    # has 4 914 candidates x rules; K covers it and the start of the second: the restatement,
+    # too, rejects every one of them
+    "c3fix": (lambda: gen.config3(), 10, 5200),
 }
 LATE_STATE = os.path.join(HERE, "c3_late_state.npz")
+STATES = {"c3late": LATE_STATE, "c3fix": os.path.join(HERE, "c3_fixpoint_state.npz")}
 
 
 def sha(a: np.ndarray) -> str:
@@ -60,13 +66,13 @@ def prepare(name):
     rng = np.random.default_rng(42)
     work, _ = engine._orient_faststmf(R, rng)
     U0 = engine.acol_means(work, rank, 5, rng).astype(work.dtype)
-    if name == "c3late":
-        U0 = np.load(LATE_STATE)["U"].astype(work.dtype)
+    if name in STATES:
+        U0 = np.load(STATES[name])["U"].astype(work.dtype)
     return work, U0, rank, K
 
 
-def late_V(work):
-    return np.load(LATE_STATE)["V"].astype(work.dtype)
+def late_V(work, name="c3late"):
+    return np.load(STATES[name])["V"].astype(work.dtype)
 
 
 def run(name):
@@ -74,8 +80,8 @@ def run(name):
     work, U0, rank, K = prepare(name)
     X = work.values
     M = work.mask
-    if name == "c3late":
-        V0 = late_V(work)
+    if name in STATES:
+        V0 = late_V(work, name)
     else:
         V0 = np.stack([oracle.residuate_row(X, M, U0[:, k]) for k in range(rank)])
     t1 = time.time()

@@ -18,7 +18,7 @@ import pytest
 from paper_2205_06619_b200 import _ext
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
-from make_golden_fp32_shapes import OUT, late_V, prepare, sha  # noqa: E402
+from make_golden_fp32_shapes import OUT, STATES, late_V, prepare, sha  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -36,22 +36,26 @@ def _check_inputs(fx, name, work, U0):
     assert str(fx[f"{name}_sha_U0"]) == sha(U0), "init drift"
 
 
-@pytest.mark.parametrize("name", ["c4s", "c3", "c3late", pytest.param("c4", marks=pytest.mark.slow)])
+@pytest.mark.parametrize("name", ["c4s", "c3", "c3late", "c3fix", pytest.param("c4", marks=pytest.mark.slow)])
 def test_capped_sweep1_prefix_matches_restatement(fx, name):
     """c3late starts from the device's state after 24 sweeps of config 3 (stored in the
-    fixtures): the restatement's next K attempts, reproduced bit for bit."""
+    fixtures): the restatement's next K attempts, reproduced bit for bit.  c3fix starts from
+    the state after sweep 41, the fit's fixpoint: the restatement and the device both reject
+    every candidate of the first row visit."""
     work, U0, rank, K = prepare(name)
     assert int(fx[f"{name}_K"]) == K
     _check_inputs(fx, name, work, U0)
     with _ext.Session(work.values, work.mask, rank) as s:
         # V0 = (-U0)^T (x)* R on the device (engine.py:194), or the stored late state's V
-        s.set_factors(U0, late_V(work) if name == "c3late" else None)
+        s.set_factors(U0, late_V(work, name) if name in STATES else None)
         assert sha(s.get_factors()[1]) == str(fx[f"{name}_sha_V0"])
         s.set_max_attempts(K)
         tt, te, cnt = s.run(budget_sweeps=1, epsilon=0.0)
         U, V = s.get_factors()
     assert cnt["attempts"] == int(fx[f"{name}_attempts"])
     assert cnt["accepts"] == int(fx[f"{name}_accepts"])
+    if name == "c3fix":
+        assert cnt["accepts"] == 0 and cnt["attempts"] == K and te[0] == te[-1] == 1353413.1359968781
     assert np.array_equal(te, fx[f"{name}_traj_e"])
     assert np.array_equal(tt, fx[f"{name}_traj_t"])
     assert np.array_equal(U[:64], fx[f"{name}_U_head"])
