@@ -2529,6 +2529,23 @@ static void launch_sampled(unsigned grid, cudaStream_t st, int64_t m, int64_t n,
                                                                             F, lim);
 }
 
+// k_maxplus_err_lanes<RQ, SPAN>: RQ = 16-byte vectors per factor row, SPAN = columns per chunk
+using LanesKernel = void (*)(int64_t, int64_t, const unsigned char*, const int64_t*, const float*, const float*, u64*,
+                             int*, int, double, int, int, int);
+template <int RQ>
+static LanesKernel lanes_kernel_span(int span) {
+  switch (span) {
+    case 2048: if constexpr (RQ == 1) return k_maxplus_err_lanes<RQ, 2048>; else return nullptr;
+    case 1024: return k_maxplus_err_lanes<RQ, 1024>;
+    case 512: return k_maxplus_err_lanes<RQ, 512>;
+    case 256: return k_maxplus_err_lanes<RQ, 256>;
+  }
+  return nullptr;
+}
+static LanesKernel lanes_kernel(int rq, int span) {
+  return rq == 1 ? lanes_kernel_span<1>(span) : rq == 2 ? lanes_kernel_span<2>(span) : lanes_kernel_span<4>(span);
+}
+
 static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint64_t seed, int reps, int flush,
                                int device, double* out, float* X_out, uint32_t* mask_out, float* U_out,
                                float* V_out, int layout = 0) {
@@ -2540,9 +2557,9 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   // the sampled layout has two kernels: lane-compacted chunks (stmf_maxplus_lanes.cuh: n a multiple of
   // 1024, rank <= 16) and the older 128 x 128 tiles.  layout 1 picks lanes when it applies
   // (STMF_C5_SAMPLED=tiles forces the tile kernel), layout 2 demands it.
-  const int ln_rq = r <= 4 ? 1 : r <= 8 ? 2 : 4, ln_sp = ln_span(ln_rq);  // (m % 128 == 0 is checked above)
-  const bool lanes_ok = n % ln_sp == 0 && m % kLnRows == 0 && r <= 16;
-  if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-coded layout: n must be a multiple of %d and rank <= 16", ln_sp);
+  // (m % 128 == 0 is checked above; n % 256 == 0 admits the narrowest chunk)
+  const bool lanes_ok = n % kLnMinSpan == 0 && m % kLnRows == 0 && r <= 16;
+  if (layout == 2 && !lanes_ok) fail(STMF_ERR_INVALID, "lane-coded layout: n must be a multiple of %d and rank <= 16", kLnMinSpan);
   bool lanes = layout == 2;
   if (layout == 1 && lanes_ok && !(getenv("STMF_C5_SAMPLED") && !strcmp(getenv("STMF_C5_SAMPLED"), "tiles"))) lanes = true;
   if (layout == 2) layout = 1;
@@ -2634,25 +2651,39 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
   u64 given_h = 0;
   DevBuf<int> lnmax;
   DevBuf<uint8_t> lnrecs;
-  int ln_cpw_log2 = 0, ln_stages = 1, ln_cap = 16;
+  int ln_cpw_log2 = 0, ln_stages = 1, ln_cap = 16, ln_sp = 0;
   size_t ln_smem = 0;
   int64_t ln_bytes = 0;
   if (layout == 1 && lanes) {
     const int RS = 4 * rq;
-    const int64_t nrc = m / kLnRows, nsp = n / ln_sp, nch = nrc * nsp;
-    tcnt.alloc(nch + 1); toff.alloc(nch + 1); lnmax.alloc(1);
-    CK(cudaMemsetAsync(tcnt.p + nch, 0, sizeof(int64_t), st));
-    CK(cudaMemsetAsync(lnmax.p, 0, sizeof(int), st));
-    k_ln_count<<<gb, 256, 0, st>>>(m, n, ln_sp, M.p, tcnt.p, lnmax.p); LAUNCH_CK();
+    // chunk width: the widest SPAN (dividing n) whose largest record fits a shared-memory stage with
+    // two blocks per SM (denser matrices get narrower chunks of about as many entries); if even the
+    // narrowest does not fit, the narrowest, with the oversized records read from global memory
+    if (const char* e = getenv("STMF_C5_STAGES")) ln_stages = std::min(kLnMaxStages, std::max(1, atoi(e)));
+    const size_t per_block = (size_t)prop.sharedMemPerMultiprocessor / 2 - 3072;  // static + reserved shared memory
+    int64_t nrc = m / kLnRows, nsp = 0, nch = 0, units = 0;
+    int maxrec = 0;
+    size_t vbytes = 0, budget = 0;
+    for (ln_sp = ln_max_span(rq); ln_sp >= kLnMinSpan; ln_sp /= 2) {
+      if (n % ln_sp) continue;
+      if (const char* e = getenv("STMF_C5_SPAN")) if (atoi(e) != ln_sp && atoi(e) >= kLnMinSpan && n % atoi(e) == 0) continue;
+      nsp = n / ln_sp; nch = nrc * nsp;
+      tcnt.alloc(nch + 1); toff.alloc(nch + 1); lnmax.alloc(1);
+      CK(cudaMemsetAsync(tcnt.p + nch, 0, sizeof(int64_t), st));
+      CK(cudaMemsetAsync(lnmax.p, 0, sizeof(int), st));
+      k_ln_count<<<gb, 256, 0, st>>>(m, n, ln_sp, M.p, tcnt.p, lnmax.p); LAUNCH_CK();
+      CK(cudaMemcpyAsync(&maxrec, lnmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      vbytes = sizeof(float4) * rq * ln_sp;
+      budget = per_block > vbytes ? per_block - vbytes : 0;
+      if ((size_t)kLnWarps * ln_stages * std::max(maxrec, 128) <= budget || ln_sp == kLnMinSpan || getenv("STMF_C5_SPAN")) break;
+    }
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt.p, toff.p, nch + 1, st));
     DevBuf<uint8_t> tmp;
     tmp.alloc(tb);
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, tcnt.p, toff.p, nch + 1, st));
-    int64_t units = 0;
-    int maxrec = 0;
     CK(cudaMemcpyAsync(&units, toff.p + nch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&maxrec, lnmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     ln_bytes = units * 16;
     lnrecs.alloc((size_t)std::max<int64_t>(ln_bytes, 16));
@@ -2661,24 +2692,19 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     Urm.alloc((size_t)m * RS); Vrm.alloc((size_t)n * RS);
     k_sp_factor<<<nblk(m * RS, 256), 256, 0, st>>>(m, r, RS, Ut.p, Urm.p); LAUNCH_CK();
     k_sp_factor<<<nblk(n * RS, 256), 256, 0, st>>>(n, r, RS, V.p, Vrm.p); LAUNCH_CK();
-    // one record in flight per warp and stage; a stage holds the largest record as long as two
-    // blocks still fit an SM beside their V spans (larger records, i.e. the densest chunks or high
-    // densities, are read straight from global memory)
-    if (const char* e = getenv("STMF_C5_STAGES")) ln_stages = std::min(kLnMaxStages, std::max(1, atoi(e)));
-    const size_t vbytes = sizeof(float4) * rq * ln_sp;
-    const size_t per_block = (size_t)prop.sharedMemPerMultiprocessor / 2 - 3072;  // static + reserved shared memory
-    const size_t budget = per_block > vbytes ? per_block - vbytes : 0;
+    // one record in flight per warp and stage
     ln_cap = std::max(maxrec, 128);
     if ((size_t)kLnWarps * ln_stages * ln_cap > budget) ln_cap = std::max<int>(128, (int)(budget / (kLnWarps * ln_stages)) & ~15);
-    const void* kf = rq == 1 ? (const void*)k_maxplus_err_lanes<1> : rq == 2 ? (const void*)k_maxplus_err_lanes<2>
-                                                                            : (const void*)k_maxplus_err_lanes<4>;
+    const void* kf = (const void*)lanes_kernel(rq, ln_sp);
+    if (!kf) fail(STMF_ERR_INVALID, "no lane-coded kernel for rank %d, span %d", r, ln_sp);
     ln_smem = vbytes + (size_t)kLnWarps * ln_stages * ln_cap;
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ln_smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 32 * kLnWarps, ln_smem));
     per_sm = std::max(per_sm, 1);
-    // chunks per warp run: 8 when that still gives every resident warp a run
-    int cpw = 8;
+    // chunks per warp run: 4 (measured: 0.630 ms vs 0.634 with 8 at 65536^2, shorter runs balance the
+    // warps better) when that still gives every resident warp a run
+    int cpw = 4;
     if (const char* e = getenv("STMF_C5_CPW")) cpw = std::max(1, atoi(e));
     while (cpw > 1 && (nrc % cpw || (nrc / cpw) * nsp < (int64_t)prop.multiProcessorCount * per_sm * kLnWarps)) cpw /= 2;
     while ((1 << ln_cpw_log2) < cpw) ln_cpw_log2++;
@@ -2690,8 +2716,8 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaStreamSynchronize(st));
     if (getenv("STMF_C5_VERBOSE"))
       fprintf(stderr, "[stmf c5] lane-coded layout: %lld chunks, records %lld bytes (+ %lld of offsets), largest %d, "
-              "stages %d x %d B, cpw %d, grid %u x 512, %d blocks/SM, smem %zu\n", (long long)nch, (long long)ln_bytes,
-              (long long)(nch + 1) * 8, maxrec, ln_stages, ln_cap, cpw, sgrid, per_sm, ln_smem);
+              "span %d, stages %d x %d B, cpw %d, grid %u x 512, %d blocks/SM, smem %zu\n", (long long)nch,
+              (long long)ln_bytes, (long long)(nch + 1) * 8, maxrec, ln_sp, ln_stages, ln_cap, cpw, sgrid, per_sm, ln_smem);
   } else if (layout == 1) {
     int RS = sp_stride(rq);
     int64_t T = (m / kSpT) * (n / kSpT);
@@ -2734,15 +2760,8 @@ static void maxplus_bench_impl(int64_t m, int64_t n, int r, double density, uint
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
     CK(cudaEventRecord(e0, st));
     if (layout == 1 && lanes) {
-      if (rq == 1)
-        k_maxplus_err_lanes<1><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
-                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
-      else if (rq == 2)
-        k_maxplus_err_lanes<2><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
-                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
-      else
-        k_maxplus_err_lanes<4><<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p, F,
-                                                            exact_limit, ln_cpw_log2, ln_stages, ln_cap);
+      lanes_kernel(rq, ln_sp)<<<sgrid, 32 * kLnWarps, ln_smem, st>>>(m, n, lnrecs.p, toff.p, Urm.p, Vrm.p, acc.p, flags.p,
+                                                                     F, exact_limit, ln_cpw_log2, ln_stages, ln_cap);
     } else if (layout == 1) {
       auto L = rq == 1 ? launch_sampled<1> : rq == 2 ? launch_sampled<2> : rq == 4 ? launch_sampled<4>
              : rq == 8 ? launch_sampled<8> : launch_sampled<16>;

@@ -461,17 +461,22 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 // entry with k among them needs all l again.  Those are ~2 / rank of the entries, so nearly
 // every warp has one, and recomputing them in place made the whole pass issue-bound on a
 // divergent path that ran with 7-13 of 32 lanes active (ncu at config 4: 8.6-14.6 warp
-// instructions per entry, 19% of HBM; profiles/r02_product2.md).  Instead each block
-// collects the entries of its tile that need the recompute in shared memory and its first
-// threads then recompute them one per lane, every lane busy.  (A global list + a second
-// kernel was tried first: the single-address atomics and the scattered second pass made
-// it slower than the divergent version.)
+// instructions per entry, 19% of HBM; profiles/r02_product2.md).  Instead every warp queues
+// the entries that need the recompute in shared memory and recomputes them 32 at a time, one
+// per lane, whenever its queue holds a full warp's worth (and the rest at the end).  No block
+// barriers, no global atomics.  (Tried first: a global list + a second kernel — the
+// single-address atomics and the scattered second pass made it slower than the divergent
+// version; then a per-block list between two barriers — 34% of HBM, a quarter of the stalls
+// at the barriers.)
 #ifndef STMF_PROD_U
 #define STMF_PROD_U 2
 #endif
 constexpr int kProdU = STMF_PROD_U;  // entries per thread and iteration, their loads issued together
+#ifndef STMF_PROD_MINB
+#define STMF_PROD_MINB 1
+#endif
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, STMF_PROD_MINB)
 k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
            int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
            const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
@@ -490,16 +495,23 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     }
     return;
   }
-  __shared__ int s_n;
-  __shared__ int32_t s_p[256 * kProdU];  // the tile's entries that need all l (N < 2^31 per device)
+  // per-warp queue of entries that need all l (entry numbers fit 32 bits: N < 2^31 per device)
+  __shared__ int32_t s_q[8][32 * (kProdU + 1)];
   const T* __restrict__ Uk = Ut + (int64_t)k * m;
   const T* __restrict__ Vk = V + (int64_t)k * n;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  int32_t* __restrict__ myq = s_q[wib];
+  int qn = 0;  // queue length (warp-uniform)
+  auto recompute = [&](int64_t q) {
+    const int64_t rr = rowof[q], cc = colof[q];
+    T n1, n2;
+    int x1, x2;
+    top2_rows(Urm + rr * rp, Vcm + cc * rp, rank, rp, n1, n2, x1, x2);
+    t1[q] = n1; t2[q] = n2; ag[q] = (uint8_t)x1; ag2[q] = (uint8_t)x2;
+  };
   const int64_t tile = (int64_t)blockDim.x * kProdU;
   for (int64_t base = blockIdx.x * tile; base < N; base += (int64_t)gridDim.x * tile) {
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
     int64_t p[kProdU];
     int32_t r[kProdU], c[kProdU];
     int a1[kProdU], a2[kProdU];
@@ -525,16 +537,11 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     }
 #pragma unroll
     for (int u = 0; u < kProdU; u++) {
-      // k held a top-2 slot: all l again, after the tile's flat part
+      // k held a top-2 slot: all l again, from the warp's queue
       const bool slow = ok[u] && (a1[u] == k || a2[u] == k);
       const unsigned bal = __ballot_sync(0xffffffffu, slow);
-      if (bal) {
-        const int leader = __ffs(bal) - 1;
-        int at = 0;
-        if (lane == leader) at = atomicAdd(&s_n, __popc(bal));
-        at = __shfl_sync(0xffffffffu, at, leader);
-        if (slow) s_p[at + __popc(bal & lt)] = (int32_t)p[u];
-      }
+      if (slow) myq[qn + __popc(bal & lt)] = (int32_t)p[u];
+      qn += __popc(bal);
       if (!ok[u] || slow) continue;
       // k held neither top-2 slot: insert its new value (lowest index on max ties);
       // most entries keep their caches and are not written back
@@ -545,18 +552,16 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
       else continue;
       t1[p[u]] = n1; t2[p[u]] = n2; ag[p[u]] = (uint8_t)x1; ag2[p[u]] = (uint8_t)x2;
     }
-    __syncthreads();
-    const int ns = s_n;
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-      const int64_t q = s_p[i];
-      const int64_t rr = rowof[q], cc = colof[q];
-      T n1, n2;
-      int x1, x2;
-      top2_rows(Urm + rr * rp, Vcm + cc * rp, rank, rp, n1, n2, x1, x2);
-      t1[q] = n1; t2[q] = n2; ag[q] = (uint8_t)x1; ag2[q] = (uint8_t)x2;
+    __syncwarp();
+    while (qn >= 32) {  // a full warp of recomputes (the queue holds fewer than 32 on loop entry)
+      qn -= 32;
+      const int64_t q = myq[qn + lane];
+      __syncwarp();
+      recompute(q);
     }
-    __syncthreads();  // s_n and s_p are reused by the next tile
   }
+  __syncwarp();
+  if (lane < qn) recompute(myq[lane]);
 }
 
 // line index of every entry of a compacted layout (CSR -> row of each entry)

@@ -12,7 +12,10 @@
 // bound by the quarter-rate bit instructions.  This layout moves the whole decode into the
 // (untimed, once per matrix) format build:
 //
-//  * A chunk = 4 rows x SPAN columns (SPAN = 2048 at rank <= 4, else 1024) is one warp's
+//  * A chunk = 4 rows x SPAN columns is one warp's unit of work; SPAN (2048 ... 256, at most
+//    1024 above rank 4) is chosen per matrix as the widest whose largest chunk record still
+//    fits a shared-memory stage, so denser matrices get narrower chunks of about the same
+//    number of entries.  (SPAN = 2048 up to ~12% density at rank <= 4.)  A chunk is one warp's
 //    unit of work.  Lane l = 8 q + j owns the given entries of row q of the chunk whose
 //    column c has c mod 8 == j; its U row lives in registers.  The span's V rows sit in
 //    shared memory in natural order (16 bytes per column and plane), so the 8 lanes of a
@@ -45,8 +48,9 @@ constexpr int kLnRows = 4;       // rows per chunk (one per quarter-warp)
 constexpr int kLnMaxStages = 2;
 constexpr int kLnWarps = 16;     // warps per block (one V span staged per block)
 constexpr int kLnHeader = 112;   // 32 u16 lane counts, total, iterations, 32 u8 lane ranks; padded to 16 bytes
-// columns per chunk: 8 column classes x 256 (rank <= 4) or x 128 codes
-__host__ __device__ constexpr int ln_span(int rq) { return rq == 1 ? 2048 : 1024; }
+// widest chunk: 8 column classes x 256 codes (rank <= 4) or x 128 (the V span must fit shared memory)
+__host__ __device__ constexpr int ln_max_span(int rq) { return rq == 1 ? 2048 : 1024; }
+constexpr int kLnMinSpan = 256;
 
 __device__ __forceinline__ void ln_mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -101,7 +105,7 @@ __device__ __forceinline__ float4 ln_lds4(unsigned a) {
 // one chunk: the record is at shared address rs (STAGED) or global pointer rg; uu = the
 // lane's U row; vlane = shared address of V column j = lane & 7 of the span (the column of
 // an entry is j + 8 * code)
-template <int RQ, bool STAGED>
+template <int RQ, int SPAN, bool STAGED>
 __device__ __forceinline__ double ln_entry(unsigned xs, unsigned cs, const unsigned char* __restrict__ xg,
                                            const unsigned char* __restrict__ cg, unsigned base,
                                            const float4 (&uu)[RQ], unsigned vlane, double part) {
@@ -111,7 +115,7 @@ __device__ __forceinline__ double ln_entry(unsigned xs, unsigned cs, const unsig
   float p0 = -CUDART_INF_F, p1 = -CUDART_INF_F;
 #pragma unroll
   for (int q = 0; q < RQ; q++) {
-    const float4 v = ln_lds4(va + q * (ln_span(RQ) * 16)), u = uu[q];
+    const float4 v = ln_lds4(va + q * (SPAN * 16)), u = uu[q];
     const float2 a = fadd2(make_float2(u.x, u.y), make_float2(v.x, v.y));
     const float2 c = fadd2(make_float2(u.z, u.w), make_float2(v.z, v.w));
     if (q == 0) {
@@ -125,7 +129,7 @@ __device__ __forceinline__ double ln_entry(unsigned xs, unsigned cs, const unsig
   return __dadd_rn(part, (double)fabsf(__fsub_rn(x, fmaxf(p0, p1))));
 }
 
-template <int RQ, bool STAGED>
+template <int RQ, int SPAN, bool STAGED>
 __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __restrict__ rg, const float4 (&uu)[RQ],
                                            unsigned vlane, int lane, double part) {
   const int cnt = (int)ln_ld_u16<STAGED>(rs + 2 * lane, rg + 2 * lane);
@@ -142,10 +146,10 @@ __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __r
   // 16 bytes, so the load stays inside the record)
   for (int it = 0; it < maxc; it += 4) {
     const uint2 b4 = ln_ld_b64<STAGED>(bs + 2 * it, bg + 2 * it);
-    if (it < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.x & 0xffffu, uu, vlane, part);
-    if (it + 1 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.x >> 16, uu, vlane, part);
-    if (it + 2 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.y & 0xffffu, uu, vlane, part);
-    if (it + 3 < cnt) part = ln_entry<RQ, STAGED>(xs, cs, xg, cg, b4.y >> 16, uu, vlane, part);
+    if (it < cnt) part = ln_entry<RQ, SPAN, STAGED>(xs, cs, xg, cg, b4.x & 0xffffu, uu, vlane, part);
+    if (it + 1 < cnt) part = ln_entry<RQ, SPAN, STAGED>(xs, cs, xg, cg, b4.x >> 16, uu, vlane, part);
+    if (it + 2 < cnt) part = ln_entry<RQ, SPAN, STAGED>(xs, cs, xg, cg, b4.y & 0xffffu, uu, vlane, part);
+    if (it + 3 < cnt) part = ln_entry<RQ, SPAN, STAGED>(xs, cs, xg, cg, b4.y >> 16, uu, vlane, part);
   }
   return part;
 }
@@ -154,12 +158,11 @@ __device__ __forceinline__ double ln_chunk(unsigned rs, const unsigned char* __r
 // with stride 4 RQ (padding -inf).  recs = the chunk records, coff[id] = start of record id in
 // 16-byte units (id = span * (m / 4) + row-chunk).  cpw = chunks per warp run (power of two
 // dividing m / 4).
-template <int RQ>
+template <int RQ, int SPAN>
 __global__ void __launch_bounds__(32 * kLnWarps, RQ <= 2 ? 2 : 1)
 k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs, const int64_t* __restrict__ coff,
                     const float* __restrict__ Urm, const float* __restrict__ Vrm, u64* __restrict__ acc,
                     int* __restrict__ flags, int F, double exact_limit, int cpw_log2, int nstage, int stage_cap) {
-  constexpr int SPAN = ln_span(RQ);
   extern __shared__ __align__(128) unsigned char ln_smem[];
   float4* Vs = reinterpret_cast<float4*>(ln_smem);  // [RQ][SPAN]
   unsigned char* stg = ln_smem + sizeof(float4) * RQ * SPAN;
@@ -252,9 +255,9 @@ k_maxplus_err_lanes(int64_t m, int64_t n, const unsigned char* __restrict__ recs
     if (bytes <= stage_cap) {
       ln_mbar_wait(&bars[wid][s], (phase >> s) & 1u);
       phase ^= 1u << s;
-      part = ln_chunk<RQ, true>(stg_s + s * stage_cap, nullptr, uu, vlane, lane, part);
+      part = ln_chunk<RQ, SPAN, true>(stg_s + s * stage_cap, nullptr, uu, vlane, lane, part);
     } else {  // a record larger than a stage: read straight from global memory
-      part = ln_chunk<RQ, false>(0, recs + meta_off[wid][s] * 16, uu, vlane, lane, part);
+      part = ln_chunk<RQ, SPAN, false>(0, recs + meta_off[wid][s] * 16, uu, vlane, lane, part);
     }
     __syncwarp();
     issue(t + nstage, s);

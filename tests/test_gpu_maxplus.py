@@ -41,7 +41,8 @@ def test_sampled_layout_matches_dense_and_restatement(m, n, r, d):
 
 
 @pytest.mark.parametrize("m,n,r,d", [(128, 2048, 4, 0.1), (256, 2048, 13, 0.3), (128, 1024, 16, 1.0),
-                                     (384, 2048, 1, 0.5), (128, 1024, 8, 0.0), (640, 4096, 3, 0.02)])
+                                     (384, 2048, 1, 0.5), (128, 1024, 8, 0.0), (640, 4096, 3, 0.02),
+                                     (128, 768, 4, 0.2), (256, 2048, 4, 0.3)])
 @pytest.mark.parametrize("stages,cpw", [(2, 8), (1, 1), (4, 2)])
 def test_lane_compacted_kernel_matches_tiles_dense_and_restatement(m, n, r, d, stages, cpw, monkeypatch):
     """k_maxplus_err_lanes (lane-coded chunk records, bulk-copy stages) against the dense kernel,
@@ -57,6 +58,19 @@ def test_lane_compacted_kernel_matches_tiles_dense_and_restatement(m, n, r, d, s
     assert b["objective"] == a["objective"] == t["objective"]
     X, M, U, V = b["data"]
     assert b["objective"] == oracle.approx_error(np.where(M, X, np.nan).astype(np.float32), M, U, V)
+
+
+@pytest.mark.parametrize("span", [256, 512, 1024, 2048])
+@pytest.mark.parametrize("r", [4, 7])
+def test_lane_coded_kernel_every_chunk_width(span, r, monkeypatch):
+    """The chunk width is chosen per matrix (the widest whose records fit a stage); every width
+    gives the same exact objective (STMF_C5_SPAN forces one; 2048 exists at rank <= 4 only)."""
+    if span == 2048 and r > 4:
+        pytest.skip("SPAN 2048 is a rank <= 4 instantiation")
+    a = _ext.bench_maxplus(256, 4096, r, 0.12, seed=41, reps=1, flush_l2=False, layout="dense")
+    monkeypatch.setenv("STMF_C5_SPAN", str(span))
+    b = _ext.bench_maxplus(256, 4096, r, 0.12, seed=41, reps=1, flush_l2=False, layout="lanes")
+    assert b["kernel"] == "k_maxplus_err_lanes" and b["objective"] == a["objective"]
 
 
 @pytest.mark.parametrize("r", [4, 16, 64])
