@@ -472,11 +472,13 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 #define STMF_PROD_U 2
 #endif
 constexpr int kProdU = STMF_PROD_U;  // entries per thread and iteration, their loads issued together
+// resident blocks per SM (binary32): the pass is bound by load latency, and 6 blocks (40 registers, no
+// spills) measured 15% faster than 4 at config 4 (profiles/r02_prod_ab.log); binary64 keeps 4 (62 registers)
 #ifndef STMF_PROD_MINB
-#define STMF_PROD_MINB 1
+#define STMF_PROD_MINB 6
 #endif
 template <typename T>
-__global__ void __launch_bounds__(256, STMF_PROD_MINB)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? STMF_PROD_MINB : 4)
 k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restrict__ colof,
            int64_t m, int64_t n, int rank, const T* __restrict__ Ut, const T* __restrict__ V,
            const T* __restrict__ Urm, const T* __restrict__ Vcm, int rp, int k, T* __restrict__ t1,
