@@ -255,6 +255,21 @@ def default_device() -> int:
     return 0
 
 
+def _host_inputs(X, mask, dtype):
+    """The arrays handed to stmf_create*: X as is (the library ignores values under the mask,
+    include/stmf_b200.h, so NaNs there need no scrubbing pass) and the boolean mask viewed as
+    bytes; copies only when the layout or dtype requires one."""
+    Xc = np.ascontiguousarray(X, dtype=dtype)
+    mask = np.asarray(mask)
+    if mask.shape != Xc.shape:
+        raise ValueError(f"mask shape {mask.shape} != value shape {Xc.shape}")
+    if mask.dtype == np.bool_ and mask.flags.c_contiguous:
+        Mc = mask.view(np.uint8)
+    else:
+        Mc = np.ascontiguousarray(mask != 0, dtype=np.uint8)
+    return Xc, Mc
+
+
 class Session:
     """One device-resident fit state (work orientation).  Owns all device buffers."""
 
@@ -262,8 +277,7 @@ class Session:
         X = np.asarray(X)
         self.dtype = np.dtype(X.dtype)
         code = dtype_code(self.dtype)
-        Xc = np.ascontiguousarray(np.where(mask, X, 0), dtype=self.dtype)
-        Mc = np.ascontiguousarray(mask, dtype=np.uint8)
+        Xc, Mc = _host_inputs(X, mask, self.dtype)
         self.m, self.n = Xc.shape
         self.rank = int(rank)
         h = _vp()
@@ -284,8 +298,7 @@ class Session:
         """Row-sharded engine with `shards` row blocks in this process (one device)."""
         self = cls.__new__(cls)
         self.dtype = np.dtype(np.float32)
-        Xc = np.ascontiguousarray(np.where(mask, X, 0), dtype=np.float32)
-        Mc = np.ascontiguousarray(mask, dtype=np.uint8)
+        Xc, Mc = _host_inputs(X, mask, np.float32)
         h = _vp()
         _check(lib().stmf_create_sim_group(ctypes.byref(h), STMF_F32, Xc.shape[0], Xc.shape[1], int(rank),
                                            _p(Xc), _p(Mc), int(shards),
@@ -300,8 +313,7 @@ class Session:
         """This process's shard of a row-sharded fit (one GPU per process, NCCL)."""
         self = cls.__new__(cls)
         self.dtype = np.dtype(np.float32)
-        Xc = np.ascontiguousarray(np.where(mask_rows, X_rows, 0), dtype=np.float32)
-        Mc = np.ascontiguousarray(mask_rows, dtype=np.uint8)
+        Xc, Mc = _host_inputs(X_rows, mask_rows, np.float32)
         starts = np.ascontiguousarray(row_starts, dtype=np.int64)
         nnz = np.ascontiguousarray(row_nnz, dtype=np.int64)
         idbuf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))

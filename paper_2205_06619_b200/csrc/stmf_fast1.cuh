@@ -141,8 +141,7 @@ struct Fast1 {
 template <typename T>
 __device__ __forceinline__ void fast1_item(const SideB<T>& S, bool ulf, int64_t it, int E,
                                            const int32_t* __restrict__ ek, const Fast1<T>& FS, int lane) {
-  constexpr int EG = kEG, P = Ilv<T>::P;
-  using V16 = typename Vec16<T>::type;
+  constexpr int EG = kEG;
   const int64_t nlines = S.nlines;
   const int ngroups = (E + EG - 1) / EG;
   const int g = (int)(it / nlines);
@@ -213,9 +212,7 @@ __device__ __forceinline__ void fast1_item(const SideB<T>& S, bool ulf, int64_t 
       kk[q] = ek[e0 + (q < ne ? q : ne - 1)];
       unif &= kk[q] == kk[0];
     }
-    const V16* pl[P];
-#pragma unroll
-    for (int p = 0; p < P; p++) pl[p] = reinterpret_cast<const V16*>(S.vin) + ((int64_t)g * P + p) * S.len_other;
+    const GroupRows<T> pl{S.vin, g, S.len_other};
     const int beg = (int)S.ptr[L], end = (int)S.ptr[L + 1];
     T mn[EG], s[EG];
     if (ulf && unif && S.inl_base) {

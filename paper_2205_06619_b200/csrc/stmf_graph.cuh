@@ -203,7 +203,7 @@ __device__ int g_chunk(DevCtl* c, const GBufs<T>& B, int cls, int scan) {
     int q = scan >> 1, op = scan & 1;
     c->ch_ev[rank] = scan; c->ch_q[rank] = q; c->ch_op[rank] = op; c->ch_cert[rank] = cls == 2;
     RepSlot<T> S;
-    constexpr int EGP = Ilv<T>::EGP;
+    constexpr int EGP = Ilv<T>::STRIDE;
     S.k = B.ck[c->t0 + q];
     if (op == 0) {
       S.a = B.ubufB + (int64_t)q * B.m; S.as = 1;

@@ -826,20 +826,31 @@ __global__ void k_scatter_row(int64_t nc, const int32_t* __restrict__ cols, cons
 }
 
 // ----------------------------------------------------------------------------
-// Phase A writes each eval's first-residuation vector in a planar eval-interleaved
-// layout  I[g][p][line][EGP]  (g = group of kEG evals, p = plane of EGP = 16 bytes
-// of evals): phase B fetches the kEG values of one given entry with kEG/EGP 16-byte
-// loads, and the 32 lanes of each load read consecutive 16-byte slots (few L1
-// wavefronts) instead of kEG scattered gathers.
+// Phase A writes each eval's first-residuation vector in an eval-interleaved layout
+// I[g][line][kEG]  (g = group of kEG evals): the kEG values of one given entry are one
+// contiguous, naturally aligned row of kEG * sizeof(T) bytes (32 at binary32, 64 at
+// binary64), fetched by phase B with 256-bit loads (LDG.E.256 on sm_100a).  A lane's
+// gather then touches ONE cache line per entry and group instead of one per 16-byte plane
+// of the earlier planar layout I[g][p][line][EGP] -- phase B at config 3 is bound by L1
+// wavefronts, and each wavefront serves one line (profiles/r02_phaseB_c3.md).
+// binary64 keeps the planar layout (its rows would be 64 bytes = two 256-bit loads, measured
+// 3% slower at config 2); binary32 measured 1.4% (config 3) to 8-11% (config 4) faster with
+// rows (profiles/r02_ilv_ab.log).  STMF_ILV_PLANAR=0 / 1 forces rows / planar for both types.
 constexpr int kEG = 8;
+#ifndef STMF_ILV_PLANAR
+#define STMF_ILV_PLANAR -1
+#endif
 
 template <typename T>
 struct Ilv {
-  static constexpr int EGP = 16 / (int)sizeof(T);
-  static constexpr int P = kEG / EGP;
+  static constexpr int EGP = 16 / (int)sizeof(T);  // evals per 16-byte vector
+  static constexpr int P = kEG / EGP;              // 16-byte vectors per entry and group
+  // element stride between consecutive lines of one eval
+  static constexpr bool PLANAR = STMF_ILV_PLANAR < 0 ? sizeof(T) == 8 : STMF_ILV_PLANAR != 0;
+  static constexpr int STRIDE = PLANAR ? EGP : kEG;
 };
 
-// one 16-byte plane slot of the interleaved layout
+// one 16-byte slot of the interleaved layout
 template <typename T> struct Vec16;
 template <> struct Vec16<float> {
   typedef float4 type;
@@ -858,19 +869,62 @@ template <> struct Vec16<double> {
 
 template <typename T>
 __host__ __device__ __forceinline__ int64_t ilv_index(int q, int64_t a, int64_t len) {
-  constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
-  int g = q / kEG, p = (q % kEG) / EGP, e = q % EGP;
-  return (((int64_t)g * P + p) * len + a) * EGP + e;
+  if constexpr (Ilv<T>::PLANAR) {
+    constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
+    int g = q / kEG, p = (q % kEG) / EGP, e = q % EGP;
+    return (((int64_t)g * P + p) * len + a) * EGP + e;
+  } else {
+    return ((int64_t)(q / kEG) * len + a) * kEG + (q % kEG);
+  }
 }
 
 template <typename T>
 __device__ __forceinline__ void ilv_decode(int64_t t, int64_t len, int& q, int64_t& a) {
-  constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
-  int e = (int)(t % EGP);
-  int64_t rest = t / EGP;
-  a = rest % len;
-  int64_t gp = rest / len;
-  q = (int)(gp / P) * kEG + (int)(gp % P) * EGP + e;
+  if constexpr (Ilv<T>::PLANAR) {
+    constexpr int EGP = Ilv<T>::EGP, P = Ilv<T>::P;
+    int e = (int)(t % EGP);
+    int64_t rest = t / EGP;
+    a = rest % len;
+    int64_t gp = rest / len;
+    q = (int)(gp / P) * kEG + (int)(gp % P) * EGP + e;
+  } else {
+    int e = (int)(t % kEG);
+    int64_t rest = t / kEG;
+    a = rest % len;
+    q = (int)(rest / len) * kEG + e;
+  }
+}
+
+// 32 bytes (256-bit load, read-only path); p must be 32-byte aligned
+__device__ __forceinline__ void ldg256(const float* p, float (&v)[8], int o = 0) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[o]), "=f"(v[o + 1]), "=f"(v[o + 2]), "=f"(v[o + 3]), "=f"(v[o + 4]), "=f"(v[o + 5]),
+                 "=f"(v[o + 6]), "=f"(v[o + 7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ldg256(const double* p, double (&v)[8], int o) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[o]), "=d"(v[o + 1]), "=d"(v[o + 2]), "=d"(v[o + 3])
+               : "l"(p));
+}
+
+// the kEG first-residuation values of line c of group g (vin = the whole buffer)
+template <typename T>
+__device__ __forceinline__ void load_group_row(const T* __restrict__ vin, int g, int64_t len, int64_t c, T (&v)[kEG]) {
+  if constexpr (Ilv<T>::PLANAR) {
+    using V16 = typename Vec16<T>::type;
+    const V16* b = reinterpret_cast<const V16*>(vin) + (int64_t)g * Ilv<T>::P * len + c;
+#pragma unroll
+    for (int p = 0; p < Ilv<T>::P; p++) Vec16<T>::unpack(__ldg(b + p * len), v, p * Ilv<T>::EGP);
+  } else {
+    const T* b = vin + ((int64_t)g * len + c) * kEG;
+    if constexpr (sizeof(T) == 4) {
+      ldg256(b, v);
+    } else {
+      ldg256(b, v, 0);
+      ldg256(b + 4, v, 4);
+    }
+  }
 }
 
 // Phase A.  F-ULF evals q: v'_c = min(CM^(-i)_c, X_ic - s_q), s_q = X_ij - V_kj
@@ -1029,7 +1083,7 @@ __global__ void k_phaseA_urf_seed_chk(int64_t m, int E, int64_t i, const int32_t
   int64_t km = (int64_t)ck[q] * m;
   T s = sub_rn(cx[q], Ut[km + i]);
   T* u = uI + ilv_index<T>(q, 0, m);
-  constexpr int EGP = Ilv<T>::EGP;
+  constexpr int EGP = Ilv<T>::STRIDE;
   for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
     int64_t r = row_idx[p] * EGP;
     u[r] = vmin(u[r], sub_rn(xc[p], s));
@@ -1053,7 +1107,7 @@ __global__ void k_phaseA_urf_seed(int64_t m, int E, int64_t i, const int32_t* __
   T s = sub_rn(cx[q], Ut[km + i]);
   T* u = uI + ilv_index<T>(q, 0, m);
   for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
-    int64_t r = row_idx[p] * Ilv<T>::EGP;
+    int64_t r = row_idx[p] * Ilv<T>::STRIDE;
     u[r] = vmin(u[r], sub_rn(xc[p], s));
   }
 }
@@ -1094,7 +1148,7 @@ struct SideB {
   const T* t1;
   const T* t2;
   const uint8_t* ag;
-  const T* vin;      // planar interleaved [g][p][len_other][EGP]: first-residuation vectors
+  const T* vin;      // eval-interleaved [g][len_other][kEG]: first-residuation vectors
   int64_t len_other;
   const T* cur;      // rank x nlines: current factor row for this side
   T* out;            // E x nlines: second residuation
@@ -1162,19 +1216,13 @@ __device__ __forceinline__ V lane_pick(const V (&a)[EG], int q) {
   return v;
 }
 
-// the kEG values of entry column c of one group (group base g, plane stride len)
-__device__ __forceinline__ void load_eg(const float* __restrict__ g, int64_t len, int64_t c, float (&v)[kEG]) {
-  float4 a = __ldg(reinterpret_cast<const float4*>(g) + c);
-  float4 b = __ldg(reinterpret_cast<const float4*>(g) + len + c);
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-__device__ __forceinline__ void load_eg(const double* __restrict__ g, int64_t len, int64_t c, double (&v)[kEG]) {
-#pragma unroll
-  for (int i = 0; i < kEG / 2; i++) {
-    double2 a = __ldg(reinterpret_cast<const double2*>(g) + i * len + c);
-    v[2 * i] = a.x; v[2 * i + 1] = a.y;
-  }
-}
+// the rows of one eval group in the phase-A buffer
+template <typename T>
+struct GroupRows {
+  const T* vin;
+  int g;
+  int64_t len;
+};
 
 // the kEG first-residuation values of entry column c for the evals of a group:
 // VM 0/1 read the planar phase-A buffer (plane pointers pl[]); VM 2 (F-ULF, one k
@@ -1182,15 +1230,14 @@ __device__ __forceinline__ void load_eg(const double* __restrict__ g, int64_t le
 // exactly as phase A does: v'_q,c = min(CM^(-i)_kc, X_ic - s_q)
 template <typename T, int VM>
 __device__ __forceinline__ void eval_vals(const T* __restrict__ xr_row, const T* __restrict__ base,
-                                          const typename Vec16<T>::type* const (&pl)[Ilv<T>::P], const T (&s)[kEG],
+                                          const GroupRows<T>& pl, const T (&s)[kEG],
                                           int c, T (&v)[kEG]) {
   if (VM == 2) {
     T b = base[c], xr = xr_row[c];
 #pragma unroll
     for (int q = 0; q < kEG; q++) v[q] = vmin(b, sub_rn(xr, s[q]));
   } else {
-#pragma unroll
-    for (int p = 0; p < Ilv<T>::P; p++) Vec16<T>::unpack(__ldg(pl[p] + c), v, p * Ilv<T>::EGP);
+    load_group_row<T>(pl.vin, pl.g, pl.len, c, v);
   }
 }
 
@@ -1225,7 +1272,7 @@ __device__ __forceinline__ V warp_reduce8(const V (&v)[kEG], int lane) {
 // (F-ULF entries whose column is not given in row i, VM 2 only): v' is the group's
 // base value for every eval, so one minimum mn0 serves all 8 evals.
 template <typename T, int VM, bool SHARED>
-__device__ __forceinline__ void pass1_seg(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+__device__ __forceinline__ void pass1_seg(const SideB<T>& S, const GroupRows<T>& pl,
                                           const T* __restrict__ base, const T (&s)[kEG], int lo, int hi, int lane,
                                           T (&mn)[kEG], T& mn0) {
   constexpr int EG = kEG;
@@ -1263,7 +1310,7 @@ __device__ __forceinline__ void pass1_seg(const SideB<T>& S, const typename Vec1
 // Pass 2 over entries [lo, hi): per-eval error partials with the new line values mn.
 // |x - max(Q, w)| == |min(x - Q, x - w)| exactly (x - . is monotone under rounding).
 template <typename T, int UNR, int VM, bool SHARED>
-__device__ __forceinline__ void pass2_seg(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+__device__ __forceinline__ void pass2_seg(const SideB<T>& S, const GroupRows<T>& pl,
                                           const T* __restrict__ base, const T (&s)[kEG], const int (&kq)[kEG],
                                           int lo, int hi, int lane, const T (&mn)[kEG], double (&part)[kEG]) {
   constexpr int EG = kEG, U2 = UNR;
@@ -1320,7 +1367,7 @@ __device__ __forceinline__ void pass2_seg(const SideB<T>& S, const typename Vec1
 // x - v' over the line's entries (pass 1), reduced over the warp; every lane ends with
 // all kEG values
 template <typename T, int VM>
-__device__ __forceinline__ void line_min8(const SideB<T>& S, const typename Vec16<T>::type* const (&pl)[Ilv<T>::P],
+__device__ __forceinline__ void line_min8(const SideB<T>& S, const GroupRows<T>& pl,
                                           const T* __restrict__ base, const T (&s)[kEG], int beg, int sp, int end,
                                           int lane, T (&mn)[kEG]) {
 #pragma unroll
@@ -1343,13 +1390,9 @@ template <typename T, int UNR, int VM>
 __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g, int e0, int ne,
                                             const int (&kq)[kEG], int lane, int* __restrict__ flags, int F,
                                             double exact_limit) {
-  constexpr int EG = kEG, P = Ilv<T>::P;
-  using V16 = typename Vec16<T>::type;
+  constexpr int EG = kEG;
   int64_t nlines = S.nlines;
-  const V16* pl[P];
-#pragma unroll
-  for (int p = 0; p < P; p++)
-    pl[p] = reinterpret_cast<const V16*>(S.vin) + ((int64_t)g * P + p) * S.len_other;
+  const GroupRows<T> pl{S.vin, g, S.len_other};
   T s[EG];
   const T* base = nullptr;
   if (VM == 2) {
@@ -1495,7 +1538,6 @@ k_phaseB_long(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, con
     int64_t nlines = S.nlines;
     int e0 = g * EG;
     int ne = E - e0 < EG ? E - e0 : EG;
-    const T* __restrict__ vg = S.vin + (int64_t)g * S.len_other * EG;
     int kq[EG];
 #pragma unroll
     for (int q = 0; q < EG; q++) kq[q] = ek[e0 + (q < ne ? q : ne - 1)];
@@ -1510,7 +1552,7 @@ k_phaseB_long(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, con
       for (int64_t p = beg + threadIdx.x; p < end; p += 256) {
         T x = S.xv[p];
         T v[EG];
-        load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+        load_group_row<T>(S.vin, g, S.len_other, (int64_t)S.idx[p], v);
 #pragma unroll
         for (int q = 0; q < EG; q++) mn[q] = vmin(mn[q], sub_rn(x, v[q]));
       }
@@ -1544,7 +1586,7 @@ k_phaseB_long(SideB<T> A, SideB<T> B, int E, const int32_t* __restrict__ ek, con
       T a1 = S.t1[p], a2 = S.t2[p];
       int a = S.ag[p];
       T v[EG];
-      load_eg(vg, S.len_other, (int64_t)S.idx[p], v);
+      load_group_row<T>(S.vin, g, S.len_other, (int64_t)S.idx[p], v);
 #pragma unroll
       for (int q = 0; q < EG; q++) {
         T Q = (a == kq[q]) ? a2 : a1;

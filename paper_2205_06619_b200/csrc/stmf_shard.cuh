@@ -128,7 +128,7 @@ __global__ void k_phaseA_urf_seed_h(int64_t ml, int E, const int32_t* __restrict
   T s = sub_rn(cx[q], urow[ck[q]]);
   T* u = uI + ilv_index<T>(q, 0, ml);
   for (int64_t p = col_ptr[j] + threadIdx.x; p < col_ptr[j + 1]; p += blockDim.x) {
-    int64_t r = row_idx[p] * Ilv<T>::EGP;
+    int64_t r = row_idx[p] * Ilv<T>::STRIDE;
     u[r] = vmin(u[r], sub_rn(xc[p], s));
   }
 }
@@ -499,8 +499,7 @@ struct ShardGroup : SessionBase {
     LAUNCH_CK();
     k_fill_csc<T><<<nblk(n, 128), 128, 0, st>>>(ml, n, dX.p, dM.p, s.col_ptr.p, s.row_idx.p, s.xc.p);
     LAUNCH_CK();
-    for (int64_t a = 0; a < ml * n; a++)
-      if (mask[a]) gridX = std::max(gridX, f32_grid((float)X[a]));
+    gridX = std::max(gridX, f32_grid_given(X, mask, ml * n));
     s.Ut.alloc((size_t)rank * ml); s.V.alloc((size_t)rank * n);
     s.t1r.alloc(Nl); s.t2r.alloc(Nl); s.agr.alloc(Nl); s.t1c.alloc(Nl); s.t2c.alloc(Nl); s.agc.alloc(Nl);
     s.a2r.alloc(Nl); s.a2c.alloc(Nl);

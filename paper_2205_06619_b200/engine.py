@@ -72,9 +72,9 @@ def random_acol_init(R: MaskedMatrix, rank: int, columns: int, rng: np.random.Ge
 def _orient_faststmf(R: MaskedMatrix, rng: np.random.Generator):
     """_SpecStrategy.orient for ByRow/RandPermR/wide (strategies.py:324-337)."""
     transposed = R.m > R.n
-    work = R.transpose() if transposed else R.copy()
-    row_perm = Permutation.random(work.m, rng)
-    work = work.permute_rows(row_perm)
+    base = R.transpose() if transposed else R  # permute_rows returns fresh arrays: no copy first
+    row_perm = Permutation.random(base.m, rng)
+    work = base.permute_rows(row_perm)
     return work, Orientation(transposed, row_perm, None)
 
 
@@ -87,7 +87,7 @@ def _orient(spec, R: MaskedMatrix, rng: np.random.Generator):
         perm = sort_perm_by_min(R, "cols")
         return R.permute_cols(perm), Orientation(col_perm=perm)
     transposed = spec.prefer_wide and R.m > R.n
-    work = R.transpose() if transposed else R.copy()
+    work = R.transpose() if transposed else R  # the permutations below return fresh arrays
     row_perm = col_perm = None
     if spec.permutation == "PermR":
         row_perm = sort_perm_by_min(work, "rows")
@@ -98,6 +98,8 @@ def _orient(spec, R: MaskedMatrix, rng: np.random.Generator):
     elif spec.permutation == "PermC":
         col_perm = sort_perm_by_min(work, "cols")
         work = work.permute_cols(col_perm)
+    elif not transposed:
+        work = R.copy()  # the fit never writes its input, but the caller's arrays stay the caller's
     return work, Orientation(transposed, row_perm, col_perm)
 
 

@@ -98,8 +98,19 @@ class MaskedMatrix:
         values = np.asarray(values, dtype=dtype)
         return cls(values, np.ones(values.shape, dtype=bool), dtype=dtype)
 
+    @classmethod
+    def _derived(cls, values: np.ndarray, mask: np.ndarray) -> "MaskedMatrix":
+        """A matrix built from fresh copies of an already validated one (copy, transpose,
+        permutation): the invariants (finite given entries, NaN under the mask) carry over,
+        so the constructor's second copy and its passes over the data are skipped -- at
+        config 3 they were 1.1 s of host time per fit (profiles/r02_e2e_host.md)."""
+        obj = cls.__new__(cls)
+        obj.values = values
+        obj.mask = mask
+        return obj
+
     def copy(self) -> "MaskedMatrix":
-        return MaskedMatrix(self.values.copy(), self.mask.copy(), dtype=self.dtype)
+        return self._derived(self.values.copy(), self.mask.copy())
 
     def validate_coverage(self):
         if self.mask.size == 0:
@@ -112,17 +123,17 @@ class MaskedMatrix:
             raise ValueError(f"column {int(np.flatnonzero(~cols)[0])} has no given entries")
 
     def transpose(self) -> "MaskedMatrix":
-        return MaskedMatrix(self.values.T.copy(), self.mask.T.copy(), dtype=self.dtype)
+        return self._derived(self.values.T.copy(), self.mask.T.copy())
 
     def permute_rows(self, p: Permutation) -> "MaskedMatrix":
         if p.size != self.m:
             raise ValueError("permutation length does not match row count")
-        return MaskedMatrix(self.values[p.forward], self.mask[p.forward], dtype=self.dtype)
+        return self._derived(self.values[p.forward], self.mask[p.forward])
 
     def permute_cols(self, p: Permutation) -> "MaskedMatrix":
         if p.size != self.n:
             raise ValueError("permutation length does not match column count")
-        return MaskedMatrix(self.values[:, p.forward], self.mask[:, p.forward], dtype=self.dtype)
+        return self._derived(self.values[:, p.forward], self.mask[:, p.forward])
 
     def row_mins(self) -> np.ndarray:
         """Per-row minimum over given entries, +inf for all-missing rows (tropical.py:141-143)."""
