@@ -465,8 +465,9 @@ def roofline(args, work, prof, step_s, clk):
     traffic = prof.get("dram_bytes")
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": prof.get("capture"),
-            "dram_frac_measured": (traffic / (prof["duration_us"] * 1e-6) / 1e9 / peak)
-            if traffic and prof.get("duration_us") else None,
+            # measured DRAM bytes per launch (launch list: one streaming of the entry data,
+            # about the same for every batch size) over the live average launch time
+            "dram_frac_measured": (traffic / avg_s / 1e9 / peak) if traffic else None,
             "kernel": "stmf::k_phaseB (candidate evaluation: 2nd residuation + error, both rules)",
             "algorithmic_bytes_per_launch": 2 * b_pass, "evals_per_launch": evaluated / nb,
             "avg_launch_us": avg_s * 1e6, "launches": nb, "share_of_step": (b_ns / 1e9) / step_s,
