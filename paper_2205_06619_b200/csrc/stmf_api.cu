@@ -1561,11 +1561,12 @@ struct Session : SessionBase {
                 : (!fixed_sched && ema_first ? depth_ema : 0.0);
     if (dd > 0)
       first = (int)std::max<int64_t>(batch_floor, std::min<int64_t>(Emax, (int64_t)(sched_scale * dd) + sched_add));
+    if (!fixed_sched) first = round_batch(first, e_round, Emax);
     int next = first;
     while (t0 < nc) {
       int E = (int)std::min<int64_t>(nc - t0, fixed_sched ? batch_sched[std::min(bi, batch_sched.size() - 1)] : next);
       bi++;
-      next = std::min(Emax, std::max(next + 1, (int)(next * sched_growth)));
+      next = round_batch(std::max(next + 1, (int)(next * sched_growth)), e_round, Emax);
       int limit = -1;
       if (max_attempts > 0) {
         int64_t rem = max_attempts - R.attempts;
@@ -1892,6 +1893,8 @@ struct Session : SessionBase {
     if (const char* e = getenv("STMF_SCHED")) sscanf(e, "%lf,%d,%lf", &sched_scale, &sched_add, &sched_growth);
   }
   int batch_floor = 1;
+  // batch sizes in whole eval groups (round_batch); STMF_EROUND=1 keeps the raw schedule
+  int e_round = getenv("STMF_EROUND") ? std::max(1, atoi(getenv("STMF_EROUND"))) : kEG;
   bool fixed_sched = false;
   bool defer_accepts = getenv("STMF_NO_DEFER") == nullptr;
 
@@ -2248,6 +2251,7 @@ struct Session : SessionBase {
       h.sweep = (double)R.cur_sweep;
       h.sched_scale = sched_scale; h.sched_growth = sched_growth; h.sched_add = sched_add;
       h.batch_floor = batch_floor; h.Emax = Emax; h.first0 = batch_sched[0];
+      h.e_round = fixed_sched ? 1 : e_round;
       h.ema_first = ema_first ? 1 : 0;
       h.depth_ema = depth_ema;
       h.cache_k = -1;

@@ -63,7 +63,7 @@ struct GBufs {
 __device__ __forceinline__ int grow_next(const DevCtl* c, int next) {
   int g = (int)(next * c->sched_growth);
   int v = next + 1 > g ? next + 1 : g;
-  return v < c->Emax ? v : c->Emax;
+  return round_batch(v, c->e_round, c->Emax);
 }
 
 __global__ void k_g_sweep_begin(DevCtl* c, int64_t m, cudaGraphConditionalHandle h_row) {
@@ -89,6 +89,7 @@ __global__ void k_g_row_begin(DevCtl* c, const int64_t* __restrict__ row_ptr, co
     if (f < c->batch_floor) f = c->batch_floor;
     first = (int)f;
   }
+  first = round_batch(first, c->e_round, c->Emax);
   c->E = (int)(nc < first ? nc : first);
   c->next = grow_next(c, first);
   cudaGraphSetConditional(h_batch, 1);

@@ -78,9 +78,18 @@ struct DevCtl {
   // schedule (Session::row_visit)
   double sched_scale, sched_growth;
   int sched_add, batch_floor, Emax, first0;
+  int e_round;  // batch sizes are rounded up to a multiple of this (kEG: whole eval groups)
   int ema_first;         // rows without depth history: first batch from depth_ema
   double depth_ema;      // running mean of accepting depths (candidates)
 };
+
+// Phase B costs a whole group of kEG evals per side whether the group is full or not, so a
+// batch of E candidates is rounded up to whole groups: the padding slots become speculative
+// evals of the next candidates instead of duplicates (same decisions in the same order).
+__host__ __device__ inline int round_batch(int e, int r, int emax) {
+  if (r > 1) e = (e + r - 1) / r * r;
+  return e < emax ? e : emax;
+}
 
 // ----------------------------------------------------------------------------
 // scalar helpers (explicit _rn intrinsics: no contraction, no fast-math)
@@ -468,14 +477,29 @@ __global__ void k_scatter_factor(int64_t len, int rp, int k, const T* __restrict
 // single-address atomics and the scattered second pass made it slower than the divergent
 // version; then a per-block list between two barriers — 34% of HBM, a quarter of the stalls
 // at the barriers.)
-#ifndef STMF_PROD_U
-#define STMF_PROD_U 2
+// 1: every thread owns 4 consecutive entries and reads each stream with one 16-byte load (config 4:
+// 2.23 -> 1.80 ms per cache refresh; profiles/r02_ab9_kpack_pvec.log); 0: 2 entries, a block apart
+#ifndef STMF_PROD_VEC
+#define STMF_PROD_VEC 1
 #endif
+#ifndef STMF_PROD_U
+#define STMF_PROD_U (STMF_PROD_VEC ? 4 : 2)
+#endif
+// 4 consecutive values of a cache stream with 16-byte loads
+__device__ __forceinline__ void load4(const float* p, float (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void load4(const double* p, double (&o)[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
 constexpr int kProdU = STMF_PROD_U;  // entries per thread and iteration, their loads issued together
-// resident blocks per SM (binary32): the pass is bound by load latency, and 6 blocks (40 registers, no
-// spills) measured 15% faster than 4 at config 4 (profiles/r02_prod_ab.log); binary64 keeps 4 (62 registers)
+// resident blocks per SM (binary32): the pass is bound by load latency.  Scalar loads: 6 blocks (40
+// registers, no spills) measured 15% faster than 4 at config 4 (profiles/r02_prod_ab.log).  Vector loads:
+// 5 blocks (48 registers, no spills; 6 would spill 96 B, 4 measured the same as 5).  binary64 keeps 4.
 #ifndef STMF_PROD_MINB
-#define STMF_PROD_MINB 6
+#define STMF_PROD_MINB (STMF_PROD_VEC ? 5 : 6)
 #endif
 template <typename T>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? STMF_PROD_MINB : 4)
@@ -519,6 +543,34 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
     int a1[kProdU], a2[kProdU];
     T b1[kProdU], b2[kProdU], s[kProdU];
     bool ok[kProdU];
+#if STMF_PROD_VEC
+    // each thread owns kProdU = 4 consecutive entries: one 16-byte load per stream (4 bytes for
+    // the index bytes) instead of four scalar ones, a warp reads 512 contiguous bytes per stream
+    static_assert(kProdU == 4, "the vector variant handles 4 consecutive entries per thread");
+    const int64_t p0 = base + (int64_t)threadIdx.x * 4;
+    if (p0 + 4 <= N) {
+      const int4 rv = *reinterpret_cast<const int4*>(rowof + p0);
+      const int4 cv = *reinterpret_cast<const int4*>(colof + p0);
+      const uchar4 av = *reinterpret_cast<const uchar4*>(ag + p0);
+      const uchar4 aw = *reinterpret_cast<const uchar4*>(ag2 + p0);
+      r[0] = rv.x; r[1] = rv.y; r[2] = rv.z; r[3] = rv.w;
+      c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+      a1[0] = av.x; a1[1] = av.y; a1[2] = av.z; a1[3] = av.w;
+      a2[0] = aw.x; a2[1] = aw.y; a2[2] = aw.z; a2[3] = aw.w;
+      load4(t1 + p0, b1);
+      load4(t2 + p0, b2);
+#pragma unroll
+      for (int u = 0; u < 4; u++) { p[u] = p0 + u; ok[u] = true; }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        p[u] = p0 + u;
+        ok[u] = p[u] < N;
+        const int64_t q = ok[u] ? p[u] : 0;
+        r[u] = rowof[q]; c[u] = colof[q]; a1[u] = ag[q]; a2[u] = ag2[q]; b1[u] = t1[q]; b2[u] = t2[q];
+      }
+    }
+#else
 #pragma unroll
     for (int u = 0; u < kProdU; u++) {
       p[u] = base + u * (int64_t)blockDim.x + threadIdx.x;
@@ -531,6 +583,7 @@ k_product2(int64_t N, const int32_t* __restrict__ rowof, const int32_t* __restri
       b1[u] = t1[q];
       b2[u] = t2[q];
     }
+#endif
 #pragma unroll
     for (int u = 0; u < kProdU; u++) {
       STMF_IDX(r[u], m);
@@ -1311,8 +1364,9 @@ __device__ __forceinline__ void pass1_seg(const SideB<T>& S, const GroupRows<T>&
 // |x - max(Q, w)| == |min(x - Q, x - w)| exactly (x - . is monotone under rounding).
 template <typename T, int UNR, int VM, bool SHARED>
 __device__ __forceinline__ void pass2_seg(const SideB<T>& S, const GroupRows<T>& pl,
-                                          const T* __restrict__ base, const T (&s)[kEG], const int (&kq)[kEG],
-                                          int lo, int hi, int lane, const T (&mn)[kEG], double (&part)[kEG]) {
+                                          const T* __restrict__ base, const T (&s)[kEG], int k0, unsigned klo,
+                                          unsigned khi, int lo, int hi, int lane, const T (&mn)[kEG],
+                                          double (&part)[kEG]) {
   constexpr int EG = kEG, U2 = UNR;
   const T* __restrict__ xv = S.xv;
   const int32_t* __restrict__ idx = S.idx;
@@ -1347,14 +1401,19 @@ __device__ __forceinline__ void pass2_seg(const SideB<T>& S, const GroupRows<T>&
     for (int u = 0; u < U2; u++) {
       if (a[u] < 0) continue;
       if (VM >= 1) {
-        T r1 = sub_rn(x[u], (a[u] == kq[0]) ? a2[u] : a1[u]);
+        T r1 = sub_rn(x[u], (a[u] == k0) ? a2[u] : a1[u]);
 #pragma unroll
         for (int q = 0; q < EG; q++)
           part[q] = __dadd_rn(part[q], (double)vabs(vmin(r1, sub_rn(x[u], add_rn(mn[q], v[u][q])))));
       } else {
+        // per-eval k: the 8 factor indices live as bytes of klo / khi (8 registers of indices
+        // spilled in this loop); a byte of the xor is zero where the entry's argmax is eval q's k
+        const unsigned ar = (unsigned)a[u] * 0x01010101u;
+        const unsigned xl = klo ^ ar, xh = khi ^ ar;
 #pragma unroll
         for (int q = 0; q < EG; q++) {
-          T Q = (a[u] == kq[q]) ? a2[u] : a1[u];
+          const bool eq = (((q < 4) ? xl : xh) & (0xffu << (8 * (q & 3)))) == 0u;
+          T Q = eq ? a2[u] : a1[u];
           T pm = vmax(Q, add_rn(mn[q], v[u][q]));
           part[q] = __dadd_rn(part[q], (double)vabs(sub_rn(x[u], pm)));
         }
@@ -1402,6 +1461,16 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   }
   const int beg = (int)S.ptr[L], end = (int)S.ptr[L + 1];
   const int sp = (VM == 2 && S.split) ? S.split[L] : beg;  // [beg, sp): shared values
+  // factor indices (< 256) packed as bytes: all the loops below need of kq
+  const int k0 = kq[0];
+  unsigned klo = 0, khi = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    klo |= (unsigned)kq[q] << (8 * q);
+    khi |= (unsigned)kq[q + 4] << (8 * q);
+  }
+  // opaque from here on: otherwise the partial ors stay live next to the packed words
+  asm volatile("" : "+r"(klo), "+r"(khi));
   T mn[EG];
   if (S.mode == 2) {
     // line values computed before this pass: the sharded F-URF all-reduced minima, or
@@ -1413,7 +1482,7 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   }
   if (lane < ne) {
     T w = lane_pick<EG>(mn, lane);
-    int kl = lane_pick<EG>(kq, lane);
+    int kl = VM == 0 ? (int)(((lane < 4 ? klo : khi) >> (8 * (lane & 3))) & 0xffu) : k0;
     if (S.mode != 2) S.out[(int64_t)(e0 + lane) * nlines + L] = w;
     if (S.mode != 1 && w != S.cur[(int64_t)kl * nlines + L]) S.chg[e0 + lane] = 1;
   }
@@ -1421,8 +1490,8 @@ __device__ __forceinline__ void phaseB_body(const SideB<T>& S, int64_t L, int g,
   double part[EG];
 #pragma unroll
   for (int q = 0; q < EG; q++) part[q] = 0.0;
-  if (VM == 2 && sp > beg) pass2_seg<T, UNR, VM, true>(S, pl, base, s, kq, beg, sp, lane, mn, part);
-  pass2_seg<T, UNR, VM, false>(S, pl, base, s, kq, sp, end, lane, mn, part);
+  if (VM == 2 && sp > beg) pass2_seg<T, UNR, VM, true>(S, pl, base, s, k0, klo, khi, beg, sp, lane, mn, part);
+  pass2_seg<T, UNR, VM, false>(S, pl, base, s, k0, klo, khi, sp, end, lane, mn, part);
   double pv = warp_reduce8<double, true>(part, lane);
   int q = (lane >> 2) & 7;
   if ((lane & 3) == 0 && q < ne) {

@@ -359,6 +359,7 @@ struct ShardGroup : SessionBase {
   std::vector<int64_t> row_depth;
   int batch_floor = 1, sched_add = 1;
   double sched_scale = 0.9, sched_growth = 1.5;
+  int e_round = getenv("STMF_EROUND") ? std::max(1, atoi(getenv("STMF_EROUND"))) : kEG;
   int gridX = -1000;
 
   ~ShardGroup() override {
@@ -878,9 +879,10 @@ struct ShardGroup : SessionBase {
     int next = row_depth[i] > 0 ? (int)std::max<int64_t>(batch_floor, std::min<int64_t>(
                                       Emax, (int64_t)(sched_scale * row_depth[i]) + sched_add))
                                 : batch_sched[0];
+    next = round_batch(next, e_round, Emax);
     while (t0 < nc) {
       int E = (int)std::min<int64_t>(nc - t0, next);
-      next = std::min(Emax, std::max(next + 1, (int)(next * sched_growth)));
+      next = round_batch(std::max(next + 1, (int)(next * sched_growth)), e_round, Emax);
       eval_batch(i, t0, E);
       hk.resize(E);
       CK(cudaMemcpyAsync(hk.data(), sh[0]->ck.p + t0, sizeof(int) * E, cudaMemcpyDeviceToHost, st));
