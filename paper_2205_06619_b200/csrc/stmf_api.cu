@@ -698,9 +698,12 @@ struct Session : SessionBase {
     // (config 4, N ~ 1e8: faster batch growth, +5% row visits/s in sweep 1; config 3,
     // N ~ 1e7: growth 1.5 is 3-6% faster per sweep; profiles/r01_sched.md)
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
+    // (late round 2: batches are whole eval groups now (round_batch), the rounding itself supplies
+    // growth, and the tuned factor drops to 1.15 at both sizes: config 3 sweep 2 6 827 -> 6 610 ms,
+    // config 4 row visits/s +12% over growth 2.0; profiles/r02_ab11_sched.log.  Before that:)
     // (round 2, config 3: growth 1.3 instead of 1.5 is 8% faster on a sweep without depth
     // history and 3-7% on sweeps 1-3 of a fit; profiles/r02_sched_c3.log)
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = N > 50000000 ? 2.0 : 1.3; }
+    else { sched_scale = 0.9; sched_add = 1; sched_growth = 1.15; }
     read_sched_env();
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();
