@@ -87,6 +87,25 @@ def test_fast_stmf_matches_reference(monkeypatch, fits, name, graph):
     assert np.array_equal(pair.U, c["U"]) and np.array_equal(pair.V, c["V"])
 
 
+@pytest.mark.parametrize("eround", ["1", "16"])
+@pytest.mark.parametrize("graph", ["1", "0"])
+@pytest.mark.parametrize("name", ["s1", "s4", "conv"])
+def test_batch_rounding_does_not_change_the_fit(monkeypatch, fits, name, graph, eround):
+    """Batch sizes are rounded up to whole eval groups (round_batch, default 8).  The raw sizes
+    (STMF_EROUND=1) and another multiple give the reference's trajectory and factors too: how the
+    candidates of a row visit are split into batches never changes a decision."""
+    monkeypatch.setenv("STMF_GRAPH", graph)
+    monkeypatch.setenv("STMF_EROUND", eround)
+    c = fit_case(fits, name)
+    R = pkg.MaskedMatrix(c["R"], c["M"])
+    cfg = pkg.RunConfig(rank=int(c["rank"]), budget_sweeps=int(c["sweeps"]), epsilon=float(c["epsilon"]),
+                        seed=int(c["seed"]))
+    pair, traj = pkg.fast_stmf(R, int(c["rank"]), cfg)
+    assert np.array_equal(np.array(traj.errors), c["traj_e"])
+    assert np.array_equal(np.array(traj.times), c["traj_t"])
+    assert np.array_equal(pair.U, c["U"]) and np.array_equal(pair.V, c["V"])
+
+
 @pytest.mark.parametrize("graph", ["1", "0"])
 def test_config1_full_100_sweeps_matches_reference_run(monkeypatch, graph):
     """BASELINE.json configs[0] exactly as the survey ran the unmodified reference
