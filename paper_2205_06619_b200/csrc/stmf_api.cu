@@ -700,10 +700,14 @@ struct Session : SessionBase {
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
     // (late round 2: batches are whole eval groups now (round_batch), the rounding itself supplies
     // growth, and the tuned factor drops to 1.15 at both sizes: config 3 sweep 2 6 827 -> 6 610 ms,
-    // config 4 row visits/s +12% over growth 2.0; profiles/r02_ab11_sched.log.  Before that:)
+    // config 4 row visits/s +12% over growth 2.0; profiles/r02_ab11_sched.log.  The first batch of a
+    // row with history covers 0.25x its previous depth, not 0.9x: in sweeps 2-5 of config 3 the depth
+    // of a row is too weakly correlated across sweeps for a large first batch to pay (59.3 -> 53.0 s
+    // for sweeps 1-5, profiles/r02_ab12_hist_scale.log), while exhausted rows (late sweeps) still
+    // finish in ~4 batches.  Before that:)
     // (round 2, config 3: growth 1.3 instead of 1.5 is 8% faster on a sweep without depth
     // history and 3-7% on sweeps 1-3 of a fit; profiles/r02_sched_c3.log)
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = 1.15; }
+    else { sched_scale = 0.25; sched_add = 1; sched_growth = 1.15; }
     read_sched_env();
     col_idx.alloc(N); row_idx.alloc(N); xr.alloc(N); xc.alloc(N);
     k_fill_csr<T><<<nblk(m * 32, 256), 256, 0, st>>>(m, n, dX.p, dM.p, row_ptr.p, col_idx.p, xr.p); LAUNCH_CK();

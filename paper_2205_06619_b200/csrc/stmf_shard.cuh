@@ -417,7 +417,7 @@ struct ShardGroup : SessionBase {
     rowbuf_bytes = off_ag + (size_t)n;
     batch_floor = (int)std::max<int64_t>(1, std::min<int64_t>(128, 8000000 / std::max<int64_t>(N, 1)));
     if (batch_floor >= 8) { sched_scale = 1.5; sched_add = 4; sched_growth = 2.0; }
-    else { sched_scale = 0.9; sched_add = 1; sched_growth = 1.15; }
+    else { sched_scale = 0.25; sched_add = 1; sched_growth = 1.15; }
     if (const char* e = getenv("STMF_SCHED")) sscanf(e, "%lf,%d,%lf", &sched_scale, &sched_add, &sched_growth);
     row_depth.assign(m, 0);
     const T* Xp = X_rows;
